@@ -1,0 +1,75 @@
+"""Build libturbofno.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2504_11681_b200.build [--force]
+
+The shared library lands next to this file (``paper_2504_11681_b200/libturbofno.so``)
+so it travels to the GPU box with the repo snapshot.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+INCLUDE = os.path.join(os.path.dirname(HERE), "include")
+OUT = os.path.join(HERE, "libturbofno.so")
+BUILD_DIR = os.path.join(HERE, "_build")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart", "shared",
+              "-Xptxas", "-v"] + ARCH
+SOURCES = ["kernels.cu", "plane2d.cu", "api.cu", "plan.cpp"]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _deps_mtime() -> float:
+    paths = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    paths += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
+    paths.append(os.path.abspath(__file__))
+    return max(os.path.getmtime(p) for p in paths)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
+        return OUT
+    os.makedirs(BUILD_DIR, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(BUILD_DIR, src + ".o")
+        path = os.path.join(CSRC, src)
+        if src.endswith(".cpp"):
+            cmd = [nvcc, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
+        else:
+            cmd = [nvcc] + NVCC_FLAGS + ["-I", INCLUDE, "-c", path, "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+        if verbose:
+            sys.stderr.write(res.stderr)
+        with open(os.path.join(BUILD_DIR, src + ".ptxas.txt"), "w") as f:
+            f.write(res.stderr)
+        objs.append(obj)
+    tmp = OUT + ".tmp"
+    cmd = [nvcc, "-shared", "--cudart", "shared"] + ARCH + ["-o", tmp] + objs + [
+        "-L/usr/local/cuda/lib64", "-lcufft", "-lcublas", "-lcudart",
+        "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    os.replace(tmp, OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

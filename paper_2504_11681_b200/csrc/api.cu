@@ -1,0 +1,511 @@
+// C ABI of libturbofno.so: validation, workspace sizing, the per-mode
+// kernel schedule of the Fourier layer, the standalone FFT / CGEMM entry
+// points and the staged (cuFFT + cuBLAS) unfused baseline.
+//
+// Layer schedule (all modes compute pipeline.run_layer's values,
+// pipeline.py:129-294; which passes cross HBM follows the mode):
+//   rank 2 stage 1   x-FFT, truncating to keep_x      (pipeline.py:150-168)
+//   stage 2          y-FFT -> CGEMM -> y-iFFT, fused per mode
+//                    (pipeline.py:185-275)
+//   rank 2 stage 3   x-iFFT, zero-padded from keep_x   (pipeline.py:277-292)
+// Rank-2 fully_fused uses the per-plane 2D kernels (plane2d.cu) when the
+// shape qualifies: 2D-FFT(plane) -> CGEMM over modes -> 2D-iFFT(plane), so
+// only the input, the output and two 1/64-size mode tensors touch HBM.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/turbofno.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "plane2d.cuh"
+
+using namespace tfno;
+
+namespace {
+
+std::mutex g_mu;
+float2* g_tw[64] = {nullptr};  // per-device master twiddle table w_{TW_MAX}^k
+
+const float2* twiddle_table(int& err) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64) {
+    err = TFNO_ECUDA;
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_tw[dev]) {
+    std::vector<float2> h(TFNO_TW_MAX);
+    for (int k = 0; k < TFNO_TW_MAX; ++k) {
+      double ang = -2.0 * M_PI * (double)k / (double)TFNO_TW_MAX;
+      h[k] = make_float2((float)cos(ang), (float)sin(ang));
+    }
+    float2* d = nullptr;
+    if (cudaMalloc(&d, sizeof(float2) * TFNO_TW_MAX) != cudaSuccess) {
+      err = TFNO_ECUDA;
+      return nullptr;
+    }
+    if (cudaMemcpy(d, h.data(), sizeof(float2) * TFNO_TW_MAX, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(d);
+      err = TFNO_ECUDA;
+      return nullptr;
+    }
+    g_tw[dev] = d;
+  }
+  err = 0;
+  return g_tw[dev];
+}
+
+bool pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? TFNO_OK : TFNO_ECUDA; }
+
+struct Geo {
+  int64_t B, H, N, dx, dy, kx, ky;
+  int rank;
+};
+
+Geo geo_of(const tfno_cfg* c) {
+  return Geo{c->batch, c->hidden_dim, c->output_dim, c->dim_x, c->dim_y, c->keep_x, c->keep_y, c->rank};
+}
+
+// ---------------- fused-rows tiling ----------------
+bool fused_tiling(int n, int keep, int N, FusedArgs& a) {
+  if (n > 4096 || keep > 1024) return false;
+  int KC = 4096 / n;
+  KC = KC < 1 ? 1 : (KC > 8 ? 8 : KC);
+  int EC = 4096 / n;
+  EC = EC < 1 ? 1 : (EC > 32 ? 32 : EC);
+  int MT = (keep + 3) / 4;
+  int ntg_max = 256 / MT;
+  if (ntg_max < 1) return false;
+  int NT = ((N + 3) / 4) * 4;
+  if (NT > 4 * ntg_max) NT = 4 * ntg_max;
+  int cap = (8192 / keep) & ~3;
+  if (cap < 1) cap = 1;
+  if (NT > cap) NT = cap;
+  if (NT < 1) NT = 1;
+  a.n = n;
+  a.keep = keep;
+  a.N = N;
+  a.KC = KC;
+  a.EC = EC;
+  a.NT = NT;
+  while (fused_smem_bytes(a) > 220 * 1024 && (a.EC > 1 || a.NT > 1)) {
+    if (a.EC > 1)
+      a.EC /= 2;
+    else
+      a.NT = a.NT > 4 ? a.NT - 4 : a.NT - 1;
+  }
+  return fused_smem_bytes(a) <= 220 * 1024;
+}
+
+// schedule decision shared by workspace sizing and the forward
+struct Sched {
+  bool staged = false, plane2d = false;
+  bool fg = false, gi = false;  // which row fusions actually run
+  bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
+  int launches = 0;
+  std::string desc;
+};
+
+Sched make_sched(const tfno_cfg* c, int mode) {
+  Sched s;
+  Geo g = geo_of(c);
+  if (mode == TFNO_STAGED) {
+    s.staged = true;
+    s.launches = 2;
+    s.desc = "cufft|truncate|cublas|pad|cufft-inv";
+    return s;
+  }
+  bool want_fg = (mode == TFNO_FUSED_FFT_GEMM || mode == TFNO_FULLY_FUSED);
+  bool want_gi = (mode == TFNO_FUSED_GEMM_IFFT || mode == TFNO_FULLY_FUSED);
+  if (g.rank == 2 && mode == TFNO_FULLY_FUSED && plane2d_supported(c)) {
+    s.plane2d = true;
+    s.need_A = s.need_C = true;
+    s.launches = 3;
+    s.desc = "plane-fft2d|cgemm-modes|plane-ifft2d";
+    return s;
+  }
+  FusedArgs fa{};
+  bool ok = fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+  s.fg = want_fg && ok;
+  s.gi = want_gi && ok;
+  s.need_s1 = s.need_mid = (g.rank == 2);
+  s.need_A = !s.fg;
+  s.need_C = !s.gi;
+  std::string d;
+  int L = 0;
+  if (g.rank == 2) {
+    d += "x-fft|";
+    ++L;
+  }
+  if (!s.fg) {
+    d += "y-fft|";
+    ++L;
+  }
+  if (s.fg || s.gi) {
+    d += s.fg && s.gi ? "fused-fft-cgemm-ifft|" : (s.fg ? "fused-fft-cgemm|" : "fused-cgemm-ifft|");
+    ++L;
+  } else {
+    d += "cgemm|";
+    ++L;
+  }
+  if (!s.gi) {
+    d += "y-ifft|";
+    ++L;
+  }
+  if (g.rank == 2) {
+    d += "x-ifft|";
+    ++L;
+  }
+  if (!d.empty()) d.pop_back();
+  s.desc = d;
+  s.launches = L;
+  return s;
+}
+
+// ---------------- staged baseline: cuFFT + cuBLAS ----------------
+struct BaselineCtx {
+  cublasHandle_t blas = nullptr;
+  std::map<std::tuple<int, int, int, int64_t>, cufftHandle> plans;
+};
+BaselineCtx g_base[64];
+
+int staged_chunk(const Geo& g) {
+  // batch chunk so that the full forward spectrum of a chunk is <= 8 GiB
+  int64_t per = g.H * g.dx * g.dy * 8;
+  int64_t cap = (8LL << 30) / (per > 0 ? per : 1);
+  if (cap < 1) cap = 1;
+  return (int)(cap < g.B ? cap : g.B);
+}
+
+size_t staged_ws(const Geo& g) {
+  int64_t bc = staged_chunk(g);
+  return (size_t)(bc * g.H * g.dx * g.dy + g.B * g.H * g.kx * g.ky + g.B * g.N * g.kx * g.ky) * 8;
+}
+
+int get_plan(int dev, int rank, int dx, int dy, int64_t batch, cufftHandle* out) {
+  auto key = std::make_tuple(rank, dx, dy, batch);
+  auto& ctx = g_base[dev];
+  auto it = ctx.plans.find(key);
+  if (it != ctx.plans.end()) {
+    *out = it->second;
+    return 0;
+  }
+  cufftHandle h;
+  if (cufftCreate(&h) != CUFFT_SUCCESS) return TFNO_ECUFFT;
+  size_t wsz = 0;
+  cufftResult r;
+  if (rank == 2) {
+    long long dims[2] = {dx, dy};
+    r = cufftMakePlanMany64(h, 2, dims, nullptr, 1, (long long)dx * dy, nullptr, 1, (long long)dx * dy, CUFFT_C2C,
+                            batch, &wsz);
+  } else {
+    long long dims[1] = {dy};
+    r = cufftMakePlanMany64(h, 1, dims, nullptr, 1, dy, nullptr, 1, dy, CUFFT_C2C, batch, &wsz);
+  }
+  if (r != CUFFT_SUCCESS) {
+    cufftDestroy(h);
+    return TFNO_ECUFFT;
+  }
+  ctx.plans[key] = h;
+  *out = h;
+  return 0;
+}
+
+int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* ws, size_t ws_bytes,
+                   cudaStream_t st) {
+  Geo g = geo_of(c);
+  if (ws_bytes < staged_ws(g)) return TFNO_EWORKSPACE;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TFNO_ECUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto& ctx = g_base[dev];
+  if (!ctx.blas) {
+    if (cublasCreate(&ctx.blas) != CUBLAS_STATUS_SUCCESS) return TFNO_ECUBLAS;
+    cublasSetMathMode(ctx.blas, CUBLAS_DEFAULT_MATH);  // true FP32, no TF32
+  }
+  const int64_t bc = staged_chunk(g);
+  float2* full = ws;
+  float2* A = full + bc * g.H * g.dx * g.dy;
+  float2* Cm = A + g.B * g.H * g.kx * g.ky;
+  const int64_t plane = g.dx * g.dy, modes = g.kx * g.ky;
+  // forward FFT + truncate, chunked over batch
+  for (int64_t b0 = 0; b0 < g.B; b0 += bc) {
+    int64_t nb = (g.B - b0 < bc) ? g.B - b0 : bc;
+    cufftHandle p;
+    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.H, &p);
+    if (e) return e;
+    cufftSetStream(p, st);
+    if (cufftExecC2C(p, (cufftComplex*)(x + b0 * g.H * plane), (cufftComplex*)full, CUFFT_FORWARD) !=
+        CUFFT_SUCCESS)
+      return TFNO_ECUFFT;
+    cudaError_t ce = launch_pad_truncate(full, nb * g.H, (int)g.dx, (int)g.dy, plane, A + b0 * g.H * modes,
+                                         (int)g.kx, (int)g.ky, modes, (int)g.kx, (int)g.ky, 1.0f, st);
+    if (ce != cudaSuccess) return TFNO_ECUDA;
+  }
+  // CGEMM over the channel axis, 1/(dx*dy) folded into alpha
+  cublasSetStream(ctx.blas, st);
+  cuComplex alpha = make_cuComplex((float)(1.0 / (double)(g.dx * g.dy)), 0.f), beta = make_cuComplex(0.f, 0.f);
+  cublasStatus_t bs = cublasCgemmStridedBatched(ctx.blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)modes, (int)g.N, (int)g.H,
+                                                &alpha, (const cuComplex*)A, (int)modes, g.H * modes,
+                                                (const cuComplex*)w, (int)g.N, 0, &beta, (cuComplex*)Cm,
+                                                (int)modes, g.N * modes, (int)g.B);
+  if (bs != CUBLAS_STATUS_SUCCESS) return TFNO_ECUBLAS;
+  // pad into y, then in-place inverse FFT over the whole output
+  cudaError_t ce = launch_pad_truncate(Cm, g.B * g.N, (int)g.kx, (int)g.ky, modes, y, (int)g.dx, (int)g.dy, plane,
+                                       (int)g.kx, (int)g.ky, 1.0f, st);
+  if (ce != cudaSuccess) return TFNO_ECUDA;
+  int64_t obc = bc * g.H / (g.N > 0 ? g.N : 1);
+  if (obc < 1) obc = 1;
+  for (int64_t b0 = 0; b0 < g.B; b0 += obc) {
+    int64_t nb = (g.B - b0 < obc) ? g.B - b0 : obc;
+    cufftHandle p;
+    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.N, &p);
+    if (e) return e;
+    cufftSetStream(p, st);
+    cufftComplex* yy = (cufftComplex*)(y + b0 * g.N * plane);
+    if (cufftExecC2C(p, yy, yy, CUFFT_INVERSE) != CUFFT_SUCCESS) return TFNO_ECUFFT;
+  }
+  return cuda_status(cudaGetLastError());
+}
+
+size_t ws_bytes_for(const tfno_cfg* c, int mode) {
+  Geo g = geo_of(c);
+  Sched s = make_sched(c, mode);
+  if (s.staged) return staged_ws(g);
+  size_t e = 0;
+  if (s.need_s1) e += g.B * g.H * g.kx * g.dy;
+  if (s.need_mid) e += g.B * g.N * g.kx * g.dy;
+  if (s.need_A) e += g.B * g.H * g.kx * g.ky;
+  if (s.need_C) e += g.B * g.N * g.kx * g.ky;
+  return e * sizeof(float2);
+}
+
+FftPencilArgs pencil_args(int n, int keep, int src_len, int64_t P, const float2* in, PencilMap im, float2* out,
+                          PencilMap om, float scale, const float2* tw) {
+  FftPencilArgs a{};
+  a.n = n;
+  a.keep = keep;
+  a.src_len = src_len;
+  a.P = P;
+  a.in = in;
+  a.im = im;
+  a.out = out;
+  a.om = om;
+  a.scale = scale;
+  a.twg = tw;
+  // coalesce across pencils when elements are strided and pencils adjacent
+  a.pencil_major = (im.es != 1 && om.es != 1) ? 1 : 0;
+  int PB = 4096 / n;
+  if (PB < 1) PB = 1;
+  if (a.pencil_major && PB > 64) PB = 64;
+  if (PB > P) PB = (int)P;
+  if (PB < 1) PB = 1;
+  a.PB = PB;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tfno_strerror(int code) {
+  switch (code) {
+    case TFNO_OK: return "ok";
+    case TFNO_EINVAL: return "invalid configuration or argument";
+    case TFNO_EUNSUPPORTED: return "unsupported shape for this build";
+    case TFNO_ECUDA: return "CUDA error (or no CUDA device)";
+    case TFNO_EWORKSPACE: return "workspace too small";
+    case TFNO_ECUFFT: return "cuFFT error";
+    case TFNO_ECUBLAS: return "cuBLAS error";
+    default: return "unknown error";
+  }
+}
+
+const char* tfno_version(void) { return "turbofno-b200 0.1.0 sm_100a"; }
+
+long long tfno_launch_count(void) { return tfno::g_launches; }
+
+uint32_t tfno_config_violations(const tfno_cfg* c, const tfno_tiles* t, int fft_batch_size) {
+  if (!c) return TFNO_V_INVALID_RANK_SHAPE;
+  uint32_t v = 0;
+  if (c->rank != 1 && c->rank != 2) v |= TFNO_V_INVALID_RANK_SHAPE;
+  if (c->batch < 1 || c->hidden_dim < 1 || c->output_dim < 1) v |= TFNO_V_INVALID_RANK_SHAPE;
+  if (!pow2(c->dim_x) || !pow2(c->dim_y)) v |= TFNO_V_NON_POWER_OF_TWO;
+  if (c->keep_x < 1 || c->keep_x > c->dim_x || c->keep_y < 1 || c->keep_y > c->dim_y)
+    v |= TFNO_V_TRUNCATION_EXCEEDS;
+  if (c->rank == 1 && (c->dim_x != 1 || c->keep_x != 1)) v |= TFNO_V_INVALID_RANK_SHAPE;
+  if (t) {
+    const int32_t* f = &t->m_tb;
+    bool pos = true;
+    for (int i = 0; i < 7; ++i) pos = pos && f[i] >= 1;
+    if (!pos) {
+      v |= TFNO_V_TILE_DIVISIBILITY;
+    } else {
+      bool div = (t->m_tb % t->m_w == 0) && (t->n_tb % t->n_w == 0) && (t->m_w % t->m_t == 0) &&
+                 (t->n_w % t->n_t == 0);
+      if (!div || (t->m_w / t->m_t) * (t->n_w / t->n_t) != 32) v |= TFNO_V_TILE_DIVISIBILITY;
+    }
+    if (t->k_tb != fft_batch_size) v |= TFNO_V_BATCH_SIZE_MISMATCH;
+  }
+  return v;
+}
+
+size_t tfno_workspace_bytes(const tfno_cfg* c, int mode, int prec) {
+  (void)prec;
+  if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
+  return ws_bytes_for(c, mode);
+}
+
+int tfno_layer_schedule(const tfno_cfg* c, int mode, int prec, char* desc, size_t len) {
+  (void)prec;
+  if (!c || mode < 0 || mode > 4 || tfno_config_violations(c, nullptr, 8)) return -1;
+  Sched s = make_sched(c, mode);
+  if (desc && len) {
+    strncpy(desc, s.desc.c_str(), len - 1);
+    desc[len - 1] = 0;
+  }
+  return s.launches;
+}
+
+int tfno_fft_execute(int n, int direction, int keep, int src_len, int64_t P, const void* in, int64_t in_P0,
+                     int64_t in_s1, int64_t in_s0, int64_t in_es, void* out, int64_t out_P0, int64_t out_s1,
+                     int64_t out_s0, int64_t out_es, void* stream) {
+  if (!pow2(n) || keep < 1 || keep > n || src_len < 1 || src_len > n || P < 0 || in_P0 < 1 || out_P0 < 1)
+    return TFNO_EINVAL;
+  if (n > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
+  if (P == 0) return TFNO_OK;
+  if (!in || !out) return TFNO_EINVAL;
+  int err = 0;
+  const float2* tw = twiddle_table(err);
+  if (err) return err;
+  FftPencilArgs a = pencil_args(n, keep, src_len, P, (const float2*)in, PencilMap{in_P0, in_s1, in_s0, in_es},
+                                (float2*)out, PencilMap{out_P0, out_s1, out_s0, out_es},
+                                direction < 0 ? 1.0f : (float)(1.0 / n), tw);
+  return cuda_status(launch_fft_pencils(a, direction < 0 ? -1 : 1, (cudaStream_t)stream));
+}
+
+int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,
+               int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
+               int64_t c_ns, int64_t c_bs, float alpha, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || batch < 0) return TFNO_EINVAL;
+  if (M == 0 || N == 0 || batch == 0) return TFNO_OK;
+  if (!A || !W || !C || batch > 65535) return TFNO_EINVAL;
+  GemmArgs g{M, N, K, batch, (const float2*)A, a_ms, a_ks, a_bs, (const float2*)W, w_ks, w_ns, w_bs,
+             (float2*)C, c_ms, c_ns, c_bs, alpha};
+  return cuda_status(launch_cgemm(g, (cudaStream_t)stream));
+}
+
+int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv, void* yv,
+                       void* wsv, size_t ws_bytes, void* stream) {
+  if (!c || mode < TFNO_STAGED || mode > TFNO_FULLY_FUSED) return TFNO_EINVAL;
+  if (tfno_config_violations(c, nullptr, 8)) return TFNO_EINVAL;
+  if (prec != TFNO_FP32 && !(prec == TFNO_TF32 || prec == TFNO_BF16)) return TFNO_EINVAL;
+  if (!xv || !wv || !yv) return TFNO_EINVAL;
+  if (c->dim_x > TFNO_TW_MAX || c->dim_y > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const float2* x = (const float2*)xv;
+  const float2* w = (const float2*)wv;
+  float2* y = (float2*)yv;
+  float2* ws = (float2*)wsv;
+  size_t need = ws_bytes_for(c, mode);
+  if (ws_bytes < need || (need && !ws)) return TFNO_EWORKSPACE;
+  Geo g = geo_of(c);
+  Sched s = make_sched(c, mode);
+  if (s.staged) return staged_forward(c, x, w, y, ws, ws_bytes, st);
+  int err = 0;
+  const float2* tw = twiddle_table(err);
+  if (err) return err;
+
+  // workspace carve-up
+  float2* p = ws;
+  float2* s1 = nullptr;
+  float2* mid = nullptr;
+  float2* A = nullptr;
+  float2* Cm = nullptr;
+  if (s.need_s1) { s1 = p; p += g.B * g.H * g.kx * g.dy; }
+  if (s.need_mid) { mid = p; p += g.B * g.N * g.kx * g.dy; }
+  if (s.need_A) { A = p; p += g.B * g.H * g.kx * g.ky; }
+  if (s.need_C) { Cm = p; p += g.B * g.N * g.kx * g.ky; }
+
+  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, st));
+
+  cudaError_t e;
+  const float2* src = x;
+  if (g.rank == 2) {
+    // stage 1: x-FFT over B*H*dy strided pencils, keep kx -> s1[B,H,kx,dy]
+    FftPencilArgs a = pencil_args((int)g.dx, (int)g.kx, (int)g.dx, g.B * g.H * g.dy, x,
+                                  PencilMap{g.dy, g.dx * g.dy, 1, g.dy}, s1, PencilMap{g.dy, g.kx * g.dy, 1, g.dy},
+                                  1.0f, tw);
+    if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+    src = s1;
+  }
+  float2* dst_mid = (g.rank == 2) ? mid : y;
+  const int64_t rows_in = g.B * g.H * g.kx, rows_out = g.B * g.N * g.kx;
+  if (!s.fg) {
+    // y-FFT of every source row -> A[B,H,kx,ky]
+    FftPencilArgs a = pencil_args((int)g.dy, (int)g.ky, (int)g.dy, rows_in, src, PencilMap{1, g.dy, 0, 1}, A,
+                                  PencilMap{1, g.ky, 0, 1}, 1.0f, tw);
+    if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+  }
+  if (s.fg || s.gi) {
+    FusedArgs fa{};
+    fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+    fa.H = (int)g.H;
+    fa.gx = (int)g.kx;
+    fa.G = g.B * g.kx;
+    fa.x = src;
+    fa.x_sb = g.H * g.kx * g.dy;
+    fa.x_sp = g.dy;
+    fa.x_sh = g.kx * g.dy;
+    fa.A = A;
+    fa.a_sb = g.H * g.kx * g.ky;
+    fa.a_sp = g.ky;
+    fa.a_sh = g.kx * g.ky;
+    fa.W = w;
+    fa.y = dst_mid;
+    fa.y_sb = g.N * g.kx * g.dy;
+    fa.y_sp = g.dy;
+    fa.y_sn = g.kx * g.dy;
+    fa.C = Cm;
+    fa.c_sb = g.N * g.kx * g.ky;
+    fa.c_sp = g.ky;
+    fa.c_sn = g.kx * g.ky;
+    fa.twg = tw;
+    fa.inv_scale = (float)(1.0 / (double)g.dy);
+    if (fa.G > 2147483647LL || (g.N + fa.NT - 1) / fa.NT > 65535) return TFNO_EUNSUPPORTED;
+    if ((e = launch_fused(fa, s.fg, s.gi, st)) != cudaSuccess) return TFNO_ECUDA;
+  } else {
+    // C[b, n, pq] = sum_h A[b, h, pq] W[h, n]
+    GemmArgs ga{g.kx * g.ky, g.N, g.H, g.B, A, 1, g.kx * g.ky, g.H * g.kx * g.ky, w, g.N, 1, 0,
+                Cm, 1, g.kx * g.ky, g.N * g.kx * g.ky, 1.0f};
+    if (g.B > 65535) return TFNO_EUNSUPPORTED;
+    if ((e = launch_cgemm(ga, st)) != cudaSuccess) return TFNO_ECUDA;
+  }
+  if (!s.gi) {
+    FftPencilArgs a = pencil_args((int)g.dy, (int)g.dy, (int)g.ky, rows_out, Cm, PencilMap{1, g.ky, 0, 1}, dst_mid,
+                                  PencilMap{1, g.dy, 0, 1}, (float)(1.0 / (double)g.dy), tw);
+    if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+  }
+  if (g.rank == 2) {
+    FftPencilArgs a = pencil_args((int)g.dx, (int)g.dx, (int)g.kx, g.B * g.N * g.dy, mid,
+                                  PencilMap{g.dy, g.kx * g.dy, 1, g.dy}, y, PencilMap{g.dy, g.dx * g.dy, 1, g.dy},
+                                  (float)(1.0 / (double)g.dx), tw);
+    if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+  }
+  return TFNO_OK;
+}
+
+}  // extern "C"

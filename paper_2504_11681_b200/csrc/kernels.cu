@@ -1,0 +1,366 @@
+// General-shape kernels of the TurboFNO layer (any power-of-two length up to
+// TFNO_TW_MAX, any keep/src_len, ragged H/N/B):
+//
+//   fft_pencils_kernel  K1/K2: batched truncating / zero-padded FFT over
+//                       pencils with arbitrary (2-level) pencil strides and
+//                       element stride: the rank-2 x-axis passes
+//                       (pipeline.py:150-168, 277-292), the unfused y passes
+//                       (pipeline.py:207-232, 236-275) and the standalone
+//                       fft.execute / batched_execute API (fft.py:258-315).
+//   cgemm_kernel        K3: strided-batched FP32 SIMT complex GEMM
+//                       (cgemm.py:83-114), k ascending.
+//   fused_rows_kernel   K4/K5/K6: the paper's fused kernel over rows
+//                       (pipeline.py:185-206 k-loop, :245-250 epilogue):
+//                       FFT of a k-chunk of channel rows straight into the
+//                       shared-memory A panel, rank-k CGEMM update of a
+//                       register accumulator, padded iFFT of the C tile from
+//                       shared memory as the epilogue.  FUSE_FFT / FUSE_IFFT
+//                       select the full or partial fusions.
+//   pad_truncate_kernel staged baseline's truncate/pad copy passes
+//                       (pipeline.py:162-166, 263-268).
+#include <cuda_runtime.h>
+
+#include "fft_engine.cuh"
+#include "kernels.cuh"
+
+namespace tfno {
+
+thread_local long long g_launches = 0;
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------------------
+// K1/K2: batched pencils
+// ------------------------------------------------------------------------
+struct GlobalPencilSrc {
+  const float2* __restrict__ ptr;
+  const int64_t* base;  // smem, per pencil in block
+  int64_t es;
+  int src_len, valid;
+  __device__ __forceinline__ float2 load(int p, int e) const {
+    if (e >= src_len || p >= valid) return make_float2(0.f, 0.f);
+    return ptr[base[p] + (int64_t)e * es];
+  }
+};
+struct GlobalPencilDst {
+  float2* __restrict__ ptr;
+  const int64_t* base;
+  int64_t es;
+  int valid;
+  __device__ __forceinline__ void store(int p, int o, float2 v) const {
+    if (p < valid) ptr[base[p] + (int64_t)o * es] = v;
+  }
+};
+
+size_t fft_pencils_smem_bytes(int n, int PB, int pm) {
+  return sizeof(float2) * (size_t)(n + 2 * smem_buf_elems(n, PB, pm)) + 2 * sizeof(int64_t) * PB;
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(256) fft_pencils_kernel(FftPencilArgs a) {
+  extern __shared__ float4 smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  const int be = smem_buf_elems(a.n, a.PB, a.pencil_major);
+  float2* buf0 = tw + a.n;
+  float2* buf1 = buf0 + be;
+  int64_t* bin = reinterpret_cast<int64_t*>(buf1 + be);
+  int64_t* bout = bin + a.PB;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  load_twiddles(tw, a.twg, a.n, tid, nthr);
+  const RadixPlan rp = make_radix_plan(a.n);
+  for (int64_t pb = (int64_t)blockIdx.x * a.PB; pb < a.P; pb += (int64_t)gridDim.x * a.PB) {
+    for (int p = tid; p < a.PB; p += nthr) {
+      int64_t pg = pb + p;
+      if (pg < a.P) {
+        bin[p] = (pg / a.im.P0) * a.im.s1 + (pg % a.im.P0) * a.im.s0;
+        bout[p] = (pg / a.om.P0) * a.om.s1 + (pg % a.om.P0) * a.om.s0;
+      }
+    }
+    __syncthreads();
+    const int valid = (int)imin64(a.PB, a.P - pb);
+    GlobalPencilSrc src{a.in, bin, a.im.es, a.src_len, valid};
+    GlobalPencilDst dst{a.out, bout, a.om.es, valid};
+    fft_block<DIR>(rp, a.PB, a.pencil_major, tid, nthr, tw, src, dst, buf0, buf1, a.keep, a.scale);
+  }
+}
+
+cudaError_t launch_fft_pencils(const FftPencilArgs& a, int dir, cudaStream_t s) {
+  size_t smem = fft_pencils_smem_bytes(a.n, a.PB, a.pencil_major);
+  int64_t blocks = (a.P + a.PB - 1) / a.PB;
+  int grid = (int)imin64(blocks, 148 * 16);
+  if (grid < 1) grid = 1;
+  cudaError_t e;
+  if (dir < 0) {
+    e = cudaFuncSetAttribute(fft_pencils_kernel<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fft_pencils_kernel<-1><<<grid, 256, smem, s>>>(a);
+  } else {
+    e = cudaFuncSetAttribute(fft_pencils_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fft_pencils_kernel<1><<<grid, 256, smem, s>>>(a);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// K3: FP32 SIMT CGEMM, C[b] = alpha * A[b] (M x K) * W[b] (K x N)
+// 64x64x8 block tile, 256 threads, 4x4 complex per thread (strided rows /
+// cols so shared-memory reads are conflict-free / broadcast).
+// ------------------------------------------------------------------------
+namespace {
+constexpr int GBM = 64, GBN = 64, GBK = 8;
+}
+
+__global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
+  __shared__ float2 As[GBK][GBM];
+  __shared__ float2 Ws[GBK][GBN];
+  const int tid = threadIdx.x;
+  const int tm = tid % 16, tn = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+  const int64_t b = blockIdx.z;
+  const float2* A = g.A + b * g.a_bs;
+  const float2* W = g.W + b * g.w_bs;
+  float2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  for (int64_t k0 = 0; k0 < g.K; k0 += GBK) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      int i = tid + r * 256;
+      int mm = i % GBM, kk = i / GBM;
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < g.M && gk < g.K) ? A[gm * g.a_ms + gk * g.a_ks] : make_float2(0.f, 0.f);
+      int nn = i % GBN;
+      int64_t gn = n0 + nn;
+      Ws[kk][nn] = (gn < g.N && gk < g.K) ? W[gk * g.w_ks + gn * g.w_ns] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      float2 av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Ws[kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cmac(acc[i][j], av[i], bv[j]);
+    }
+    __syncthreads();
+  }
+  float2* C = g.C + b * g.c_bs;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t gm = m0 + tm + 16 * i;
+    if (gm >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t gn = n0 + tn + 16 * j;
+      if (gn < g.N) C[gm * g.c_ms + gn * g.c_ns] = cscale(acc[i][j], g.alpha);
+    }
+  }
+}
+
+cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid((unsigned)((g.M + GBM - 1) / GBM), (unsigned)((g.N + GBN - 1) / GBN), (unsigned)g.batch);
+  cgemm_kernel<<<grid, 256, 0, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------
+// K4/K5/K6: fused rows kernel
+// ------------------------------------------------------------------------
+struct RowSrc {  // global rows, contiguous, full length
+  const float2* __restrict__ base;
+  int64_t sh;
+  __device__ __forceinline__ float2 load(int p, int e) const { return base[(int64_t)p * sh + e]; }
+};
+struct PanelDst {  // A panel As[k][q]
+  float2* as;
+  int keep;
+  __device__ __forceinline__ void store(int p, int o, float2 v) const { as[p * keep + o] = v; }
+};
+struct ColSrc {  // C tile columns Cs[j][q], zero beyond keep
+  const float2* cs;
+  int keep, c0;
+  __device__ __forceinline__ float2 load(int p, int e) const {
+    return e < keep ? cs[(c0 + p) * keep + e] : make_float2(0.f, 0.f);
+  }
+};
+struct RowDst {  // global output rows
+  float2* __restrict__ base;
+  int64_t sn;
+  int c0;
+  __device__ __forceinline__ void store(int p, int o, float2 v) const { base[(int64_t)(c0 + p) * sn + o] = v; }
+};
+
+size_t fused_smem_bytes(const FusedArgs& a) {
+  int PB = a.KC > a.EC ? a.KC : a.EC;
+  size_t e = (size_t)a.n + 2 * (size_t)smem_buf_elems(a.n, PB, 0) + (size_t)a.KC * a.keep +
+             (size_t)a.KC * a.NT + (size_t)a.NT * a.keep;
+  return e * sizeof(float2);
+}
+
+template <bool FUSE_FFT, bool FUSE_IFFT>
+__global__ void __launch_bounds__(256) fused_rows_kernel(FusedArgs a) {
+  extern __shared__ float4 smem_raw[];
+  const int n = a.n, keep = a.keep;
+  const int PB = a.KC > a.EC ? a.KC : a.EC;
+  const int be = smem_buf_elems(n, PB, 0);
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* buf0 = tw + n;
+  float2* buf1 = buf0 + be;
+  float2* As = buf1 + be;
+  float2* Ws = As + a.KC * keep;
+  float2* Cs = Ws + a.KC * a.NT;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int64_t g = blockIdx.x;
+  const int64_t bb = g / a.gx, pp = g % a.gx;
+  const int n0 = blockIdx.y * a.NT;
+  const int ntc = min(a.NT, a.N - n0);
+  const int MT = (keep + 3) / 4, NTg = (a.NT + 3) / 4;
+  const bool gemm_thread = tid < MT * NTg;
+  const int tm = tid % MT, tn = tid / MT;
+  if (FUSE_FFT || FUSE_IFFT) load_twiddles(tw, a.twg, n, tid, nthr);
+  const RadixPlan rp = make_radix_plan(n);
+  float2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  __syncthreads();
+
+  for (int kc = 0; kc < a.H; kc += a.KC) {
+    const int kcn = min(a.KC, a.H - kc);
+    for (int i = tid; i < a.KC * a.NT; i += nthr) {
+      int k = i / a.NT, j = i % a.NT;
+      Ws[i] = (k < kcn && j < ntc) ? a.W[(int64_t)(kc + k) * a.N + n0 + j] : make_float2(0.f, 0.f);
+    }
+    if (FUSE_FFT) {
+      // rows of channels kc..kc+kcn -> FFT (keep) -> A panel in smem
+      RowSrc src{a.x + bb * a.x_sb + pp * a.x_sp + (int64_t)kc * a.x_sh, a.x_sh};
+      fft_block<-1>(rp, kcn, 0, tid, nthr, tw, src, PanelDst{As, keep}, buf0, buf1, keep, 1.0f);
+      if (kcn < a.KC) {
+        for (int i = tid; i < (a.KC - kcn) * keep; i += nthr) As[kcn * keep + i] = make_float2(0.f, 0.f);
+        __syncthreads();
+      }
+    } else {
+      const float2* Ab = a.A + bb * a.a_sb + pp * a.a_sp + (int64_t)kc * a.a_sh;
+      for (int i = tid; i < a.KC * keep; i += nthr) {
+        int k = i / keep, q = i % keep;
+        As[i] = k < kcn ? Ab[(int64_t)k * a.a_sh + q] : make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+    }
+    if (gemm_thread) {
+      for (int k = 0; k < a.KC; ++k) {
+        float2 av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int q = tm + MT * i;
+          av[i] = q < keep ? As[k * keep + q] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int c = tn + NTg * j;
+          bv[j] = c < a.NT ? Ws[k * a.NT + c] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cmac(acc[i][j], av[i], bv[j]);
+      }
+    }
+    __syncthreads();
+  }
+
+  if (FUSE_IFFT) {
+    if (gemm_thread) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int q = tm + MT * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int c = tn + NTg * j;
+          if (q < keep && c < a.NT) Cs[c * keep + q] = acc[i][j];
+        }
+      }
+    }
+    __syncthreads();
+    float2* ybase = a.y + bb * a.y_sb + pp * a.y_sp + (int64_t)n0 * a.y_sn;
+    for (int c0 = 0; c0 < ntc; c0 += a.EC) {
+      int pb = min(a.EC, ntc - c0);
+      fft_block<1>(rp, pb, 0, tid, nthr, tw, ColSrc{Cs, keep, c0}, RowDst{ybase, a.y_sn, c0}, buf0, buf1, n,
+                   a.inv_scale);
+    }
+  } else {
+    if (gemm_thread) {
+      float2* cbase = a.C + bb * a.c_sb + pp * a.c_sp + (int64_t)n0 * a.c_sn;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int q = tm + MT * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int c = tn + NTg * j;
+          if (q < keep && c < ntc) cbase[(int64_t)c * a.c_sn + q] = acc[i][j];
+        }
+      }
+    }
+  }
+}
+
+template <bool F, bool I>
+static cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
+  size_t smem = fused_smem_bytes(a);
+  cudaError_t e =
+      cudaFuncSetAttribute(fused_rows_kernel<F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)a.G, (unsigned)((a.N + a.NT - 1) / a.NT));
+  fused_rows_kernel<F, I><<<grid, 256, smem, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s) {
+  if (fuse_fft && fuse_ifft) return launch_fused_t<true, true>(a, s);
+  if (fuse_fft) return launch_fused_t<true, false>(a, s);
+  if (fuse_ifft) return launch_fused_t<false, true>(a, s);
+  return launch_fused_t<false, false>(a, s);
+}
+
+// ------------------------------------------------------------------------
+// staged baseline copy passes: dst[plane][x][y] = x<cx && y<cy ? scale*src : 0
+// ------------------------------------------------------------------------
+__global__ void pad_truncate_kernel(const float2* __restrict__ src, int64_t planes, int sx, int sy,
+                                    int64_t s_plane, float2* __restrict__ dst, int dx2, int dy2,
+                                    int64_t d_plane, int cx, int cy, float scale) {
+  const int64_t per = (int64_t)dx2 * dy2;
+  const int64_t total = planes * per;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pl = i / per;
+    int r = (int)(i % per);
+    int xx = r / dy2, yy = r % dy2;
+    float2 v = make_float2(0.f, 0.f);
+    if (xx < cx && yy < cy && xx < sx && yy < sy) v = cscale(src[pl * s_plane + (int64_t)xx * sy + yy], scale);
+    dst[pl * d_plane + (int64_t)xx * dy2 + yy] = v;
+  }
+}
+
+cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane, float2* dst,
+                                int dx2, int dy2, int64_t d_plane, int cx, int cy, float scale,
+                                cudaStream_t s) {
+  int64_t total = planes * dx2 * (int64_t)dy2;
+  int grid = (int)imin64((total + 255) / 256, 148 * 32);
+  if (grid < 1) grid = 1;
+  pad_truncate_kernel<<<grid, 256, 0, s>>>(src, planes, sx, sy, s_plane, dst, dx2, dy2, d_plane, cx, cy, scale);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tfno

@@ -1,0 +1,68 @@
+// Kernel argument structs and launch helpers shared by kernels.cu / api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tfno {
+
+// Pencil p of a batched transform starts at (p / P0) * s1 + (p % P0) * s0 and
+// its element e lives at base + e * es (all in complex elements).
+struct PencilMap {
+  int64_t P0, s1, s0, es;
+};
+
+struct FftPencilArgs {
+  int n, keep, src_len, PB, pencil_major;
+  int64_t P;
+  float scale;
+  const float2* in;
+  PencilMap im;
+  float2* out;
+  PencilMap om;
+  const float2* twg;
+};
+
+struct GemmArgs {
+  int64_t M, N, K, batch;
+  const float2* A;
+  int64_t a_ms, a_ks, a_bs;
+  const float2* W;
+  int64_t w_ks, w_ns, w_bs;
+  float2* C;
+  int64_t c_ms, c_ns, c_bs;
+  float alpha;
+};
+
+// Row-fused layer kernel (FFT along contiguous rows -> CGEMM over the
+// channel axis -> padded iFFT along rows).  A "row group" g = b*gx + p owns
+// H input rows (one per channel h) and N output rows.
+struct FusedArgs {
+  int n, keep, H, N, gx;
+  int64_t G;
+  const float2* x;
+  int64_t x_sb, x_sp, x_sh;  // input row (g,h): x + b*x_sb + p*x_sp + h*x_sh
+  const float2* A;
+  int64_t a_sb, a_sp, a_sh;  // A panel row (g,h), contiguous keep
+  const float2* W;           // [H][N] row-major
+  float2* y;
+  int64_t y_sb, y_sp, y_sn;  // output row (g,n), contiguous n
+  float2* C;
+  int64_t c_sb, c_sp, c_sn;  // C row (g,n), contiguous keep
+  int NT, KC, EC;
+  const float2* twg;
+  float inv_scale;
+};
+
+size_t fused_smem_bytes(const FusedArgs& a);
+size_t fft_pencils_smem_bytes(int n, int PB, int pencil_major);
+
+cudaError_t launch_fft_pencils(const FftPencilArgs& a, int dir, cudaStream_t s);
+cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s);
+cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
+cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,
+                                float2* dst, int dx2, int dy2, int64_t d_plane, int cx, int cy,
+                                float scale, cudaStream_t s);
+
+extern thread_local long long g_launches;  // our kernels launched by this thread
+
+}  // namespace tfno

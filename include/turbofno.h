@@ -116,6 +116,11 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
  * kernels of the staged baseline, cuFFT/cuBLAS, are not counted). */
 long long tfno_launch_count(void);
 
+/* Profiling hook (calling thread): when events != NULL, tfno_layer_forward
+ * records events[0] before its first launch and events[i+1] after its i-th
+ * stage, on its stream (cudaEvent_t handles; count = capacity). */
+void tfno_set_stage_events(void** events, int count);
+
 /* Kernel schedule tfno_layer_forward will use: number of launches and a
  * short description (e.g. "x-fft|fused-rows|x-ifft").  desc may be NULL. */
 int tfno_layer_schedule(const tfno_cfg* cfg, int mode, int prec, char* desc, size_t desc_len);

@@ -34,6 +34,18 @@ using namespace tfno;
 namespace {
 
 std::mutex g_mu;
+
+// optional per-stage profiling events (tfno_set_stage_events)
+thread_local cudaEvent_t* t_events = nullptr;
+thread_local int t_nevents = 0;
+thread_local int t_mark = 0;
+inline void stage_begin(cudaStream_t st) {
+  t_mark = 0;
+  if (t_nevents > 0) cudaEventRecord(t_events[t_mark++], st);
+}
+inline void stage_mark(cudaStream_t st) {
+  if (t_mark < t_nevents) cudaEventRecord(t_events[t_mark++], st);
+}
 float2* g_tw[64] = {nullptr};  // per-device master twiddle table w_{TW_MAX}^k
 
 const float2* twiddle_table(int& err) {
@@ -241,6 +253,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   float2* A = full + bc * g.H * g.dx * g.dy;
   float2* Cm = A + g.B * g.H * g.kx * g.ky;
   const int64_t plane = g.dx * g.dy, modes = g.kx * g.ky;
+  stage_begin(st);
   // forward FFT + truncate, chunked over batch
   for (int64_t b0 = 0; b0 < g.B; b0 += bc) {
     int64_t nb = (g.B - b0 < bc) ? g.B - b0 : bc;
@@ -255,6 +268,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
                                          (int)g.kx, (int)g.ky, modes, (int)g.kx, (int)g.ky, 1.0f, st);
     if (ce != cudaSuccess) return TFNO_ECUDA;
   }
+  stage_mark(st);
   // CGEMM over the channel axis, 1/(dx*dy) folded into alpha
   cublasSetStream(ctx.blas, st);
   cuComplex alpha = make_cuComplex((float)(1.0 / (double)(g.dx * g.dy)), 0.f), beta = make_cuComplex(0.f, 0.f);
@@ -263,6 +277,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
                                                 (const cuComplex*)w, (int)g.N, 0, &beta, (cuComplex*)Cm,
                                                 (int)modes, g.N * modes, (int)g.B);
   if (bs != CUBLAS_STATUS_SUCCESS) return TFNO_ECUBLAS;
+  stage_mark(st);
   // pad into y, then in-place inverse FFT over the whole output
   cudaError_t ce = launch_pad_truncate(Cm, g.B * g.N, (int)g.kx, (int)g.ky, modes, y, (int)g.dx, (int)g.dy, plane,
                                        (int)g.kx, (int)g.ky, 1.0f, st);
@@ -278,6 +293,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
     cufftComplex* yy = (cufftComplex*)(y + b0 * g.N * plane);
     if (cufftExecC2C(p, yy, yy, CUFFT_INVERSE) != CUFFT_SUCCESS) return TFNO_ECUFFT;
   }
+  stage_mark(st);
   return cuda_status(cudaGetLastError());
 }
 
@@ -337,6 +353,11 @@ const char* tfno_strerror(int code) {
 const char* tfno_version(void) { return "turbofno-b200 0.1.0 sm_100a"; }
 
 long long tfno_launch_count(void) { return tfno::g_launches; }
+
+void tfno_set_stage_events(void** events, int count) {
+  t_events = (cudaEvent_t*)events;
+  t_nevents = events ? count : 0;
+}
 
 uint32_t tfno_config_violations(const tfno_cfg* c, const tfno_tiles* t, int fft_batch_size) {
   if (!c) return TFNO_V_INVALID_RANK_SHAPE;
@@ -440,7 +461,8 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   if (s.need_A) { A = p; p += g.B * g.H * g.kx * g.ky; }
   if (s.need_C) { Cm = p; p += g.B * g.N * g.kx * g.ky; }
 
-  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, st));
+  stage_begin(st);
+  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, st, &stage_mark));
 
   cudaError_t e;
   const float2* src = x;
@@ -450,6 +472,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
                                   PencilMap{g.dy, g.dx * g.dy, 1, g.dy}, s1, PencilMap{g.dy, g.kx * g.dy, 1, g.dy},
                                   1.0f, tw);
     if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
     src = s1;
   }
   float2* dst_mid = (g.rank == 2) ? mid : y;
@@ -459,6 +482,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     FftPencilArgs a = pencil_args((int)g.dy, (int)g.ky, (int)g.dy, rows_in, src, PencilMap{1, g.dy, 0, 1}, A,
                                   PencilMap{1, g.ky, 0, 1}, 1.0f, tw);
     if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
   }
   if (s.fg || s.gi) {
     FusedArgs fa{};
@@ -487,23 +511,27 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     fa.inv_scale = (float)(1.0 / (double)g.dy);
     if (fa.G > 2147483647LL || (g.N + fa.NT - 1) / fa.NT > 65535) return TFNO_EUNSUPPORTED;
     if ((e = launch_fused(fa, s.fg, s.gi, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
   } else {
     // C[b, n, pq] = sum_h A[b, h, pq] W[h, n]
     GemmArgs ga{g.kx * g.ky, g.N, g.H, g.B, A, 1, g.kx * g.ky, g.H * g.kx * g.ky, w, g.N, 1, 0,
                 Cm, 1, g.kx * g.ky, g.N * g.kx * g.ky, 1.0f};
     if (g.B > 65535) return TFNO_EUNSUPPORTED;
     if ((e = launch_cgemm(ga, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
   }
   if (!s.gi) {
     FftPencilArgs a = pencil_args((int)g.dy, (int)g.dy, (int)g.ky, rows_out, Cm, PencilMap{1, g.ky, 0, 1}, dst_mid,
                                   PencilMap{1, g.dy, 0, 1}, (float)(1.0 / (double)g.dy), tw);
     if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
   }
   if (g.rank == 2) {
     FftPencilArgs a = pencil_args((int)g.dx, (int)g.dx, (int)g.kx, g.B * g.N * g.dy, mid,
                                   PencilMap{g.dy, g.kx * g.dy, 1, g.dy}, y, PencilMap{g.dy, g.dx * g.dy, 1, g.dy},
                                   (float)(1.0 / (double)g.dx), tw);
     if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+    stage_mark(st);
   }
   return TFNO_OK;
 }

@@ -1,9 +1,499 @@
+// Per-plane 2D Fourier-layer kernels for sm_100a (rank-2 fully_fused fast path).
+//
+// The reference runs rank 2 as x-FFT (own pass) -> fused y-FFT/CGEMM/y-iFFT
+// -> x-iFFT (own pass) (pipeline.py:149-292), which streams the truncated
+// stage-1 spectrum and the pre-x-iFFT output through HBM (2.5x the
+// input+output bytes at keep/dim = 1/8).  Here each persistent CTA owns whole
+// (b, channel) planes:
+//
+//   plane_fwd2d   x[b,h] (dx*dy) -> A[b,h,kx,ky]: every row streams into a
+//                 shared-memory ring with TMA bulk copies (cp.async.bulk +
+//                 mbarrier); a team of dy/8 threads does the truncated row
+//                 FFT (radix-8 in registers, smem transpose, radix-8 +
+//                 warp-shuffle transposed reduction) into the class buffer;
+//                 the x direction is a four-step transform: rows x = x0 + R*x1
+//                 (R = dx/kx) form class x0, whose kx-point column FFT is
+//                 twiddled by w_dx^{p*x0} and accumulated in registers.
+//   cgemm         C[b,n,p,q] = sum_h A[b,h,p,q] W[h,n] / (dx*dy)  (kernels.cu)
+//   plane_inv2d   C[b,n] (kx*ky) -> y[b,n] (dx*dy): per class x0, twiddle +
+//                 kx-point column iFFT gives rows x0 + R*x1 at ky bins; each
+//                 row's padded iFFT (radix-8, smem transpose, radix-8) is
+//                 written to a smem staging ring and TMA bulk-stored.
+//
+// Only x, y and the two mode tensors (kx*ky/(dx*dy) = 1/64 of a plane for
+// C3/C4) touch HBM.  Math: SURVEY.md Appendix A; row FFT decomposition
+// X[r+8t] = sum_a w_M^{ta} sum_c w_8^{tc} w_N^{r(a+Ac)} Z[a+Ac, r],
+// Z[y1, r] = sum_{y2} w_8^{r y2} x[y1 + M y2], M = N/8, A = M/8.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
 #include "plane2d.cuh"
 
 namespace tfno {
-bool plane2d_supported(const tfno_cfg*) { return false; }
-cudaError_t launch_plane2d_layer(const tfno_cfg*, const float2*, const float2*, float2*, float2*, float2*,
-                                 const float2*, int, cudaStream_t) {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float2 shfl_xor2(float2 v, int m) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+// ---------------------------------------------------------------- geometry
+template <int DX_, int KX_, int NY_, int KY_, int NTH_>
+struct PlaneGeo {
+  static constexpr int DX = DX_, KX = KX_, NY = NY_, KY = KY_, NTH = NTH_;
+  static constexpr int M = NY / 8;  // threads per row team
+  static constexpr int A = M / 8;
+  static constexpr int T = (KY + 7) / 8;
+  static constexpr int LOGA = (A >= 16 ? 4 : A >= 8 ? 3 : A >= 4 ? 2 : A >= 2 ? 1 : 0);
+  static constexpr int LOGT = (T >= 8 ? 3 : T >= 4 ? 2 : T >= 2 ? 1 : 0);
+  static constexpr int TEAMS = NTH / M;  // rows per iteration
+  static constexpr int R = DX / KX;      // four-step classes along x
+  static constexpr int KA = KX / 8;      // kx = 8 * KA
+  static constexpr int IPC = KX / TEAMS; // iterations per class
+  static constexpr int PAD = ((-7 * A) % 16 + 16) % 16;
+  static constexpr int TS = M + PAD;     // transposed-row stride
+  static constexpr int TASKS2 = (8 * KY + NTH - 1) / NTH;
+  static_assert(A >= 1 && (1 << LOGA) == A, "A power of two");
+  static_assert((1 << LOGT) == T && T <= A && T <= 8, "ky <= 8*min(8, dy/64)");
+  static_assert(8 * T == KY, "ky multiple of 8");
+  static_assert(KX % 8 == 0 && KA <= 8 && KX % TEAMS == 0 && DX % KX == 0, "kx shape");
+  static_assert(NTH % M == 0 && (M % 32 == 0 || 32 % M == 0), "team shape");
+};
+
+template <int KA, int DIR>
+__device__ __forceinline__ void dft_small(float2* v) {
+  dft<KA, DIR>(v);
+}
+
+// ============================================================== forward
+template <class G, int S>
+__global__ void __launch_bounds__(G::NTH, 1)
+    plane_fwd2d_kernel(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes,
+                       const float2* __restrict__ twg) {
+  constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
+  constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* ring = reinterpret_cast<float2*>(smem);
+  float2* tr = ring + S * TEAMS * NY;
+  float2* Tc = tr + TEAMS * 8 * TS;
+  float2* twy = Tc + KX * KY;
+  float2* twx = twy + NY;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(twx + DX);
+
+  const int tid = threadIdx.x;
+  const int team = tid / M, tt = tid % M;
+  const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t NIT = nmine * R * IPC;
+
+  for (int k = tid; k < NY; k += NTH) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]);
+  for (int k = tid; k < DX; k += NTH) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+
+  auto issue = [&](int64_t it) {
+    const int slot = (int)(it % S);
+    const int64_t pl = blockIdx.x + (it / (R * IPC)) * gridDim.x;
+    const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
+    const float2* src = x + pl * (int64_t)DX * NY;
+    float2* dst = ring + slot * TEAMS * NY;
+    mbar_expect_tx(&bars[slot], TEAMS * NY * 8);
+#pragma unroll 1
+    for (int tm = 0; tm < TEAMS; ++tm) {
+      const int row = x0 + R * (j * TEAMS + tm);
+      tma_load_1d(dst + tm * NY, src + (int64_t)row * NY, NY * 8, &bars[slot], pol);
+    }
+  };
+  if (tid == 0)
+    for (int64_t it = 0; it < S - 1 && it < NIT; ++it) issue(it);
+
+  float2 acc[G::TASKS2][KA];
+#pragma unroll
+  for (int a = 0; a < G::TASKS2; ++a)
+#pragma unroll
+    for (int u = 0; u < KA; ++u) acc[a][u] = make_float2(0.f, 0.f);
+
+  float2* trt = tr + team * 8 * TS;
+  const int a_ = tt % A, r_ = tt / A;
+  for (int64_t it = 0; it < NIT; ++it) {
+    if (tid == 0 && it + S - 1 < NIT) issue(it + S - 1);
+    const int slot = (int)(it % S);
+    mbar_wait(&bars[slot], (uint32_t)((it / S) & 1));
+    const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
+    // ---- row stage 1: radix-8 over y2, twiddle w_N^{r*y1}, transpose
+    {
+      const float2* row = ring + slot * TEAMS * NY + team * NY;
+      float2 v[8];
+#pragma unroll
+      for (int y2 = 0; y2 < 8; ++y2) v[y2] = row[tt + M * y2];
+      dft8<-1>(v);
+#pragma unroll
+      for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twy[r * tt]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) trt[r * TS + tt] = v[r];
+    }
+    __syncthreads();
+    // ---- row stage 2: radix-8 over c, twiddle w_M^{t*a}, reduce over a
+    {
+      float2 u[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) u[c] = trt[r_ * TS + a_ + A * c];
+      dft8<-1>(u);
+#pragma unroll
+      for (int t = 1; t < T; ++t) u[t] = cmul(u[t], twy[8 * t * a_]);
+      int nv = T;
+#pragma unroll
+      for (int m = A / 2; m >= 1; m >>= 1) {
+        if (nv > 1) {
+          const bool up = (a_ & m) != 0;
+          const int h = nv / 2;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < h) {
+              float2 send = up ? u[q] : u[q + h];
+              float2 keep = up ? u[q + h] : u[q];
+              float2 got = shfl_xor2(send, m);
+              u[q] = cadd(keep, got);
+            }
+          }
+          nv = h;
+        } else {
+          u[0] = cadd(u[0], shfl_xor2(u[0], m));
+        }
+      }
+      constexpr int SH = G::LOGA - G::LOGT;
+      if ((a_ & ((1 << SH) - 1)) == 0) {
+        const int t = a_ >> SH;
+        const int x1 = j * TEAMS + team;
+        Tc[x1 * KY + r_ + 8 * t] = u[0];
+      }
+    }
+    __syncthreads();
+    if (j == IPC - 1) {
+      // ---- class x0 complete: kx-point column FFT, pass 1 (radix 8 over m)
+      for (int tau = tid; tau < KA * KY; tau += NTH) {
+        const int q = tau % KY, i = tau / KY;
+        float2 v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = Tc[(i + KA * m) * KY + q];
+        dft8<-1>(v);
+#pragma unroll
+        for (int s = 1; s < 8; ++s) v[s] = cmul(v[s], twx[i * s * R]);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) Tc[(s * KA + i) * KY + q] = v[s];
+      }
+      __syncthreads();
+      // pass 2 (radix KA over i) + four-step twiddle w_dx^{p*x0}, accumulate
+#pragma unroll
+      for (int jj = 0; jj < G::TASKS2; ++jj) {
+        const int tau = tid + jj * NTH;
+        if (tau < 8 * KY) {
+          const int q = tau % KY, s = tau / KY;
+          float2 w[KA];
+#pragma unroll
+          for (int i = 0; i < KA; ++i) w[i] = Tc[(s * KA + i) * KY + q];
+          dft_small<KA, -1>(w);
+#pragma unroll
+          for (int u = 0; u < KA; ++u) {
+            const int p = s + 8 * u;
+            cmac(acc[jj][u], w[u], twx[p * x0]);
+          }
+        }
+      }
+      __syncthreads();
+      if (x0 == R - 1) {
+        const int64_t pl = blockIdx.x + (it / (R * IPC)) * gridDim.x;
+        float2* dst = Aout + pl * (int64_t)KX * KY;
+#pragma unroll
+        for (int jj = 0; jj < G::TASKS2; ++jj) {
+          const int tau = tid + jj * NTH;
+          if (tau < 8 * KY) {
+            const int q = tau % KY, s = tau / KY;
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+              dst[(s + 8 * u) * KY + q] = acc[jj][u];
+              acc[jj][u] = make_float2(0.f, 0.f);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ============================================================== inverse
+template <class G, int SO>
+__global__ void __launch_bounds__(G::NTH, 1)
+    plane_inv2d_kernel(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes,
+                       const float2* __restrict__ twg) {
+  constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
+  constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* cin = reinterpret_cast<float2*>(smem);  // 2 x KX*KY
+  float2* Gb = cin + 2 * KX * KY;                  // KX*KY
+  float2* tr = Gb + KX * KY;
+  float2* ost = tr + TEAMS * 8 * TS;               // SO x TEAMS*NY
+  float2* twy = ost + SO * TEAMS * NY;
+  float2* twx = twy + NY;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(twx + DX);
+
+  const int tid = threadIdx.x;
+  const int team = tid / M, tt = tid % M;
+  const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  for (int k = tid; k < NY; k += NTH) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]));
+  for (int k = tid; k < DX; k += NTH) twx[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]));
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol_in = policy_evict_first(), pol_out = policy_evict_first();
+  auto issue = [&](int64_t k) {
+    const int64_t pl = blockIdx.x + k * gridDim.x;
+    mbar_expect_tx(&bars[k & 1], KX * KY * 8);
+    tma_load_1d(cin + (k & 1) * KX * KY, Cin + pl * (int64_t)KX * KY, KX * KY * 8, &bars[k & 1], pol_in);
+  };
+  if (tid == 0 && nmine > 0) issue(0);
+
+  float2* trt = tr + team * 8 * TS;
+  const int a_ = tt % A, r_ = tt / A;
+  int64_t gi = 0;  // global row-iteration counter (staging ring)
+  for (int64_t k = 0; k < nmine; ++k) {
+    if (tid == 0 && k + 1 < nmine) issue(k + 1);
+    mbar_wait(&bars[k & 1], (uint32_t)((k >> 1) & 1));
+    const float2* C = cin + (k & 1) * KX * KY;
+    const int64_t pl = blockIdx.x + k * gridDim.x;
+    float2* yp = y + pl * (int64_t)DX * NY;
+    for (int x0 = 0; x0 < R; ++x0) {
+      // ---- column iFFT, pass 1: twiddle w_dx^{+p x0}, radix KA over u
+      for (int tau = tid; tau < 8 * KY; tau += NTH) {
+        const int q = tau % KY, s = tau / KY;
+        float2 w[KA];
+#pragma unroll
+        for (int u = 0; u < KA; ++u) {
+          const int p = s + 8 * u;
+          w[u] = cmul(C[p * KY + q], twx[p * x0]);
+        }
+        dft_small<KA, 1>(w);
+#pragma unroll
+        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twx[s * i * R]);
+#pragma unroll
+        for (int i = 0; i < KA; ++i) Gb[(s * KA + i) * KY + q] = w[i];
+      }
+      __syncthreads();
+      // pass 2: radix 8 over s -> rows x1 = i + KA*m (in place per task)
+      for (int tau = tid; tau < KA * KY; tau += NTH) {
+        const int q = tau % KY, i = tau / KY;
+        float2 v[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) v[s] = Gb[(s * KA + i) * KY + q];
+        dft8<1>(v);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KY + q] = v[m];
+      }
+      __syncthreads();
+      for (int j = 0; j < IPC; ++j, ++gi) {
+        const int x1 = j * TEAMS + team;
+        // ---- row stage A: twiddle w_M^{+t a}, radix 8 over t (t < T nonzero)
+        {
+          float2 u[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t < T) {
+              float2 g = Gb[x1 * KY + r_ + 8 * t];
+              u[t] = t ? cmul(g, twy[8 * t * a_]) : g;
+            } else {
+              u[t] = make_float2(0.f, 0.f);
+            }
+          }
+          dft8<1>(u);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) trt[r_ * TS + a_ + A * c] = u[c];
+        }
+        const int slot = (int)(gi % SO);
+        if (tid == 0) bulk_wait_read<SO - 1>();
+        __syncthreads();
+        // ---- row stage B: twiddle w_N^{+r y1}, radix 8 over r -> staging row
+        {
+          float2 v[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) v[r] = trt[r * TS + tt];
+#pragma unroll
+          for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twy[r * tt]);
+          dft8<1>(v);
+          float2* o = ost + slot * TEAMS * NY + team * NY;
+#pragma unroll
+          for (int y2 = 0; y2 < 8; ++y2) o[tt + M * y2] = v[y2];
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll 1
+          for (int tm = 0; tm < TEAMS; ++tm) {
+            const int row = x0 + R * (j * TEAMS + tm);
+            tma_store_1d(yp + (int64_t)row * NY, ost + slot * TEAMS * NY + tm * NY, NY * 8, pol_out);
+          }
+          bulk_commit();
+        }
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------- dispatch
+template <class G>
+constexpr size_t fwd_smem(int S) {
+  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * G::TS + G::KX * G::KY + G::NY + G::DX) +
+         8 * S + 64;
+}
+template <class G>
+constexpr size_t inv_smem(int SO) {
+  return sizeof(float2) * (3 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS + (size_t)SO * G::TEAMS * G::NY +
+                           G::NY + G::DX) +
+         16 + 64;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <class G, int S, int SO>
+static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
+                            const float2* tw, cudaStream_t st, void (*mark)(cudaStream_t)) {
+  const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
+  const int sms = num_sms();
+  // forward planes
+  {
+    size_t smem = fwd_smem<G>(S);
+    cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t planes = B * H;
+    int grid = (int)(planes < sms ? planes : sms);
+    plane_fwd2d_kernel<G, S><<<grid, G::NTH, smem, st>>>(x, A, planes, tw);
+    ++g_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (mark) mark(st);
+  }
+  // channel mixing over modes, 1/(dx*dy) folded into alpha
+  {
+    const int64_t MQ = (int64_t)G::KX * G::KY;
+    GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ,
+                (float)(1.0 / ((double)G::DX * G::NY))};
+    cudaError_t e = launch_cgemm(ga, st);
+    if (e != cudaSuccess) return e;
+    if (mark) mark(st);
+  }
+  // inverse planes
+  {
+    size_t smem = inv_smem<G>(SO);
+    cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t planes = B * N;
+    int grid = (int)(planes < sms ? planes : sms);
+    plane_inv2d_kernel<G, SO><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw);
+    ++g_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (mark) mark(st);
+  }
+  return cudaSuccess;
+}
+
+using G512 = PlaneGeo<512, 64, 512, 64, 512>;
+using G256a = PlaneGeo<256, 32, 256, 32, 512>;
+using G256b = PlaneGeo<256, 16, 256, 16, 512>;
+using G128 = PlaneGeo<128, 16, 128, 16, 256>;
+
+static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
+static_assert(inv_smem<G512>(2) <= 227 * 1024, "smem");
+
+bool plane2d_supported(const tfno_cfg* c) {
+  if (c->rank != 2 || c->batch * (int64_t)c->hidden_dim > (1LL << 40)) return false;
+  const int dx = c->dim_x, dy = c->dim_y, kx = c->keep_x, ky = c->keep_y;
+  return (dx == 512 && dy == 512 && kx == 64 && ky == 64) || (dx == 256 && dy == 256 && kx == 32 && ky == 32) ||
+         (dx == 256 && dy == 256 && kx == 16 && ky == 16) || (dx == 128 && dy == 128 && kx == 16 && ky == 16);
+}
+
+cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
+                                 float2* Cm, const float2* tw, int prec, cudaStream_t st,
+                                 void (*mark)(cudaStream_t)) {
+  (void)prec;
+  const int dx = c->dim_x, kx = c->keep_x;
+  if (dx == 512) return run_pair<G512, 3, 2>(c, x, w, y, A, Cm, tw, st, mark);
+  if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);
+  if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);
+  if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);
   return cudaErrorNotSupported;
 }
+
 }  // namespace tfno

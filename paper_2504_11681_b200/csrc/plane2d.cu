@@ -121,50 +121,95 @@ __device__ __forceinline__ void dft_small(float2* v) {
   dft<KA, DIR>(v);
 }
 
+// ---------------------------------------------------------------- sync helpers
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// row-team barrier: a team is M = dy/8 threads (one warp or less -> __syncwarp)
+template <int M>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (M <= 32)
+    __syncwarp();
+  else
+    named_bar(1 + team, M);
+}
+constexpr int kComputeBar = 15;
+
 // ============================================================== forward
+// Warp-specialised: warp NTH/32 is the TMA producer (ring of S slots, full /
+// empty mbarriers); the NTH compute threads form row teams that synchronise
+// only inside the team, plus one compute-wide barrier per class (column pass).
 template <class G, int S>
-__global__ void __launch_bounds__(G::NTH, 1)
+__global__ void __launch_bounds__(G::NTH + 32, 1)
     plane_fwd2d_kernel(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes,
                        const float2* __restrict__ twg) {
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
+  constexpr int RT = T + 2;               // padded t-stride of the reduction buffer
+  constexpr int RS = A * RT + 8;          // per-r stride (bank-conflict-free 16B stores / 8B loads)
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);
   float2* tr = ring + S * TEAMS * NY;
-  float2* Tc = tr + TEAMS * 8 * TS;
+  float2* red = tr + TEAMS * 8 * TS;
+  float2* Tc = red + TEAMS * 8 * RS;
   float2* twy = Tc + KX * KY;
   float2* twx = twy + NY;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(twx + DX);
+  uint64_t* full = reinterpret_cast<uint64_t*>(twx + DX);
+  uint64_t* empty = full + S;
 
   const int tid = threadIdx.x;
-  const int team = tid / M, tt = tid % M;
   const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t NIT = nmine * R * IPC;
 
-  for (int k = tid; k < NY; k += NTH) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]);
-  for (int k = tid; k < DX; k += NTH) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]);
+  for (int k = tid; k < NY; k += blockDim.x) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]);
+  for (int k = tid; k < DX; k += blockDim.x) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]);
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NTH / 32);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  const uint64_t pol = policy_evict_first();
 
-  auto issue = [&](int64_t it) {
-    const int slot = (int)(it % S);
-    const int64_t pl = blockIdx.x + (it / (R * IPC)) * gridDim.x;
-    const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
-    const float2* src = x + pl * (int64_t)DX * NY;
-    float2* dst = ring + slot * TEAMS * NY;
-    mbar_expect_tx(&bars[slot], TEAMS * NY * 8);
+  if (tid >= NTH) {
+    // ---------------- producer warp: stream the plane rows, class by class
+    if (tid == NTH) {
+      const uint64_t pol = policy_evict_first();
+      for (int64_t it = 0; it < NIT; ++it) {
+        const int slot = (int)(it % S);
+        if (it >= S) mbar_wait(&empty[slot], (uint32_t)(((it / S) - 1) & 1));
+        const int64_t pl = blockIdx.x + (it / (R * IPC)) * gridDim.x;
+        const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
+        const float2* src = x + pl * (int64_t)DX * NY;
+        float2* dst = ring + slot * TEAMS * NY;
+        mbar_expect_tx(&full[slot], TEAMS * NY * 8);
 #pragma unroll 1
-    for (int tm = 0; tm < TEAMS; ++tm) {
-      const int row = x0 + R * (j * TEAMS + tm);
-      tma_load_1d(dst + tm * NY, src + (int64_t)row * NY, NY * 8, &bars[slot], pol);
+        for (int tm = 0; tm < TEAMS; ++tm) {
+          const int row = x0 + R * (j * TEAMS + tm);
+          tma_load_1d(dst + tm * NY, src + (int64_t)row * NY, NY * 8, &full[slot], pol);
+        }
+      }
     }
-  };
-  if (tid == 0)
-    for (int64_t it = 0; it < S - 1 && it < NIT; ++it) issue(it);
+    return;
+  }
+
+  // ---------------- compute threads
+  const int team = tid / M, tt = tid % M;
+  const int a_ = tt % A, r_ = tt / A;
+  float2* trt = tr + team * 8 * TS;
+  float2* redt = red + team * 8 * RS;
+  // per-thread constant twiddles (a strided table walk is an 8-way bank conflict)
+  float2 tw1[8], tw2[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) tw1[r] = twy[r * tt];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) tw2[t] = twy[(8 * t * a_) % NY];
+  // reduction reader role: output storage column q' = tt = t' + T*r'
+  const int tq = tt % T, rq = tt / T;
 
   float2 acc[G::TASKS2][KA];
 #pragma unroll
@@ -172,13 +217,10 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
     for (int u = 0; u < KA; ++u) acc[a][u] = make_float2(0.f, 0.f);
 
-  float2* trt = tr + team * 8 * TS;
-  const int a_ = tt % A, r_ = tt / A;
   for (int64_t it = 0; it < NIT; ++it) {
-    if (tid == 0 && it + S - 1 < NIT) issue(it + S - 1);
     const int slot = (int)(it % S);
-    mbar_wait(&bars[slot], (uint32_t)((it / S) & 1));
     const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
+    mbar_wait(&full[slot], (uint32_t)((it / S) & 1));
     // ---- row stage 1: radix-8 over y2, twiddle w_N^{r*y1}, transpose
     {
       const float2* row = ring + slot * TEAMS * NY + team * NY;
@@ -186,49 +228,43 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
       for (int y2 = 0; y2 < 8; ++y2) v[y2] = row[tt + M * y2];
       dft8<-1>(v);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
 #pragma unroll
-      for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twy[r * tt]);
+      for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
 #pragma unroll
       for (int r = 0; r < 8; ++r) trt[r * TS + tt] = v[r];
     }
-    __syncthreads();
-    // ---- row stage 2: radix-8 over c, twiddle w_M^{t*a}, reduce over a
+    team_sync<M>(team);
+    // ---- row stage 2: radix-8 over c, twiddle w_M^{t*a} -> reduction buffer
     {
       float2 u[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) u[c] = trt[r_ * TS + a_ + A * c];
       dft8<-1>(u);
 #pragma unroll
-      for (int t = 1; t < T; ++t) u[t] = cmul(u[t], twy[8 * t * a_]);
-      int nv = T;
+      for (int t = 1; t < T; ++t) u[t] = cmul(u[t], tw2[t]);
+      float2* dst = redt + r_ * RS + a_ * RT;
+      if constexpr (T % 2 == 0) {
 #pragma unroll
-      for (int m = A / 2; m >= 1; m >>= 1) {
-        if (nv > 1) {
-          const bool up = (a_ & m) != 0;
-          const int h = nv / 2;
+        for (int t = 0; t < T; t += 2)
+          *reinterpret_cast<float4*>(dst + t) = make_float4(u[t].x, u[t].y, u[t + 1].x, u[t + 1].y);
+      } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < h) {
-              float2 send = up ? u[q] : u[q + h];
-              float2 keep = up ? u[q + h] : u[q];
-              float2 got = shfl_xor2(send, m);
-              u[q] = cadd(keep, got);
-            }
-          }
-          nv = h;
-        } else {
-          u[0] = cadd(u[0], shfl_xor2(u[0], m));
-        }
-      }
-      constexpr int SH = G::LOGA - G::LOGT;
-      if ((a_ & ((1 << SH) - 1)) == 0) {
-        const int t = a_ >> SH;
-        const int x1 = j * TEAMS + team;
-        Tc[x1 * KY + r_ + 8 * t] = u[0];
+        for (int t = 0; t < T; ++t) dst[t] = u[t];
       }
     }
-    __syncthreads();
+    team_sync<M>(team);
+    // ---- sum over a: X[r + 8t] for the thread's storage column q' = tt
+    if (tt < KY) {
+      float2 sacc = redt[rq * RS + tq];
+#pragma unroll
+      for (int a = 1; a < A; ++a) sacc = cadd(sacc, redt[rq * RS + a * RT + tq]);
+      const int x1 = j * TEAMS + team;
+      Tc[x1 * KY + tt] = sacc;
+    }
     if (j == IPC - 1) {
+      named_bar(kComputeBar, NTH);
       // ---- class x0 complete: kx-point column FFT, pass 1 (radix 8 over m)
       for (int tau = tid; tau < KA * KY; tau += NTH) {
         const int q = tau % KY, i = tau / KY;
@@ -237,40 +273,39 @@ __global__ void __launch_bounds__(G::NTH, 1)
         for (int m = 0; m < 8; ++m) v[m] = Tc[(i + KA * m) * KY + q];
         dft8<-1>(v);
 #pragma unroll
-        for (int s = 1; s < 8; ++s) v[s] = cmul(v[s], twx[i * s * R]);
+        for (int s2 = 1; s2 < 8; ++s2) v[s2] = cmul(v[s2], twx[i * s2 * R]);
 #pragma unroll
-        for (int s = 0; s < 8; ++s) Tc[(s * KA + i) * KY + q] = v[s];
+        for (int s2 = 0; s2 < 8; ++s2) Tc[(s2 * KA + i) * KY + q] = v[s2];
       }
-      __syncthreads();
+      named_bar(kComputeBar, NTH);
       // pass 2 (radix KA over i) + four-step twiddle w_dx^{p*x0}, accumulate
 #pragma unroll
       for (int jj = 0; jj < G::TASKS2; ++jj) {
         const int tau = tid + jj * NTH;
         if (tau < 8 * KY) {
-          const int q = tau % KY, s = tau / KY;
+          const int q = tau % KY, s2 = tau / KY;
           float2 w[KA];
 #pragma unroll
-          for (int i = 0; i < KA; ++i) w[i] = Tc[(s * KA + i) * KY + q];
+          for (int i = 0; i < KA; ++i) w[i] = Tc[(s2 * KA + i) * KY + q];
           dft_small<KA, -1>(w);
 #pragma unroll
-          for (int u = 0; u < KA; ++u) {
-            const int p = s + 8 * u;
-            cmac(acc[jj][u], w[u], twx[p * x0]);
-          }
+          for (int u = 0; u < KA; ++u) cmac(acc[jj][u], w[u], twx[(s2 + 8 * u) * x0]);
         }
       }
-      __syncthreads();
+      named_bar(kComputeBar, NTH);
       if (x0 == R - 1) {
+        // mode tensor in storage order (q' = t + T*r); the mode GEMM is
+        // order-agnostic and the inverse reads the same order back
         const int64_t pl = blockIdx.x + (it / (R * IPC)) * gridDim.x;
         float2* dst = Aout + pl * (int64_t)KX * KY;
 #pragma unroll
         for (int jj = 0; jj < G::TASKS2; ++jj) {
           const int tau = tid + jj * NTH;
           if (tau < 8 * KY) {
-            const int q = tau % KY, s = tau / KY;
+            const int q = tau % KY, s2 = tau / KY;
 #pragma unroll
             for (int u = 0; u < KA; ++u) {
-              dst[(s + 8 * u) * KY + q] = acc[jj][u];
+              dst[(s2 + 8 * u) * KY + q] = acc[jj][u];
               acc[jj][u] = make_float2(0.f, 0.f);
             }
           }
@@ -281,6 +316,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
 }
 
 // ============================================================== inverse
+// Row teams run decoupled (team barriers only); each team's elected thread
+// TMA-stores its own finished rows from a per-team staging ring.
 template <class G, int SO>
 __global__ void __launch_bounds__(G::NTH, 1)
     plane_inv2d_kernel(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes,
@@ -288,13 +325,13 @@ __global__ void __launch_bounds__(G::NTH, 1)
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
   extern __shared__ __align__(128) uint8_t smem[];
-  float2* cin = reinterpret_cast<float2*>(smem);  // 2 x KX*KY
-  float2* Gb = cin + 2 * KX * KY;                  // KX*KY
+  float2* ost = reinterpret_cast<float2*>(smem);  // TEAMS x SO x NY (TMA store sources)
+  float2* cin = ost + TEAMS * SO * NY;            // KX*KY (TMA load target)
+  float2* Gb = cin + KX * KY;                     // KX*KY
   float2* tr = Gb + KX * KY;
-  float2* ost = tr + TEAMS * 8 * TS;               // SO x TEAMS*NY
-  float2* twy = ost + SO * TEAMS * NY;
+  float2* twy = tr + TEAMS * 8 * TS;
   float2* twx = twy + NY;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(twx + DX);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(twx + DX);
 
   const int tid = threadIdx.x;
   const int team = tid / M, tt = tid % M;
@@ -303,56 +340,62 @@ __global__ void __launch_bounds__(G::NTH, 1)
   for (int k = tid; k < NY; k += NTH) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]));
   for (int k = tid; k < DX; k += NTH) twx[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]));
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  const uint64_t pol_in = policy_evict_first(), pol_out = policy_evict_first();
+  const uint64_t pol = policy_evict_first();
   auto issue = [&](int64_t k) {
     const int64_t pl = blockIdx.x + k * gridDim.x;
-    mbar_expect_tx(&bars[k & 1], KX * KY * 8);
-    tma_load_1d(cin + (k & 1) * KX * KY, Cin + pl * (int64_t)KX * KY, KX * KY * 8, &bars[k & 1], pol_in);
+    mbar_expect_tx(bar, KX * KY * 8);
+    tma_load_1d(cin, Cin + pl * (int64_t)KX * KY, KX * KY * 8, bar, pol);
   };
   if (tid == 0 && nmine > 0) issue(0);
 
   float2* trt = tr + team * 8 * TS;
+  float2* ostt = ost + team * SO * NY;
   const int a_ = tt % A, r_ = tt / A;
-  int64_t gi = 0;  // global row-iteration counter (staging ring)
+  const bool elected = (tt == 0);
+  float2 tw1[8], tw2[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) tw1[r] = twy[r * tt];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) tw2[t] = twy[(8 * t * a_) % NY];
+  int64_t gi = 0;  // team-local row-iteration counter (staging ring)
   for (int64_t k = 0; k < nmine; ++k) {
-    if (tid == 0 && k + 1 < nmine) issue(k + 1);
-    mbar_wait(&bars[k & 1], (uint32_t)((k >> 1) & 1));
-    const float2* C = cin + (k & 1) * KX * KY;
+    mbar_wait(bar, (uint32_t)(k & 1));
     const int64_t pl = blockIdx.x + k * gridDim.x;
     float2* yp = y + pl * (int64_t)DX * NY;
     for (int x0 = 0; x0 < R; ++x0) {
+      named_bar(kComputeBar, NTH);  // previous class's rows are done with Gb
       // ---- column iFFT, pass 1: twiddle w_dx^{+p x0}, radix KA over u
       for (int tau = tid; tau < 8 * KY; tau += NTH) {
-        const int q = tau % KY, s = tau / KY;
+        const int q = tau % KY, s2 = tau / KY;
         float2 w[KA];
 #pragma unroll
         for (int u = 0; u < KA; ++u) {
-          const int p = s + 8 * u;
-          w[u] = cmul(C[p * KY + q], twx[p * x0]);
+          const int p = s2 + 8 * u;
+          w[u] = cmul(cin[p * KY + q], twx[p * x0]);
         }
         dft_small<KA, 1>(w);
 #pragma unroll
-        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twx[s * i * R]);
+        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twx[s2 * i * R]);
 #pragma unroll
-        for (int i = 0; i < KA; ++i) Gb[(s * KA + i) * KY + q] = w[i];
+        for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KY + q] = w[i];
       }
-      __syncthreads();
+      named_bar(kComputeBar, NTH);
+      if (x0 == R - 1 && tid == 0 && k + 1 < nmine) issue(k + 1);  // cin fully consumed
       // pass 2: radix 8 over s -> rows x1 = i + KA*m (in place per task)
       for (int tau = tid; tau < KA * KY; tau += NTH) {
         const int q = tau % KY, i = tau / KY;
         float2 v[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) v[s] = Gb[(s * KA + i) * KY + q];
+        for (int s2 = 0; s2 < 8; ++s2) v[s2] = Gb[(s2 * KA + i) * KY + q];
         dft8<1>(v);
 #pragma unroll
         for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KY + q] = v[m];
       }
-      __syncthreads();
+      named_bar(kComputeBar, NTH);
       for (int j = 0; j < IPC; ++j, ++gi) {
         const int x1 = j * TEAMS + team;
         // ---- row stage A: twiddle w_M^{+t a}, radix 8 over t (t < T nonzero)
@@ -361,8 +404,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             if (t < T) {
-              float2 g = Gb[x1 * KY + r_ + 8 * t];
-              u[t] = t ? cmul(g, twy[8 * t * a_]) : g;
+              float2 g = Gb[x1 * KY + t + T * r_];  // storage column q' = t + T*r
+              u[t] = t ? cmul(g, tw2[t]) : g;
             } else {
               u[t] = make_float2(0.f, 0.f);
             }
@@ -372,45 +415,43 @@ __global__ void __launch_bounds__(G::NTH, 1)
           for (int c = 0; c < 8; ++c) trt[r_ * TS + a_ + A * c] = u[c];
         }
         const int slot = (int)(gi % SO);
-        if (tid == 0) bulk_wait_read<SO - 1>();
-        __syncthreads();
+        if (elected) bulk_wait_read<SO - 1>();  // staging slot free again
+        team_sync<M>(team);
         // ---- row stage B: twiddle w_N^{+r y1}, radix 8 over r -> staging row
         {
           float2 v[8];
 #pragma unroll
           for (int r = 0; r < 8; ++r) v[r] = trt[r * TS + tt];
 #pragma unroll
-          for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twy[r * tt]);
+          for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
           dft8<1>(v);
-          float2* o = ost + slot * TEAMS * NY + team * NY;
+          float2* o = ostt + slot * NY;
 #pragma unroll
           for (int y2 = 0; y2 < 8; ++y2) o[tt + M * y2] = v[y2];
         }
         fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-#pragma unroll 1
-          for (int tm = 0; tm < TEAMS; ++tm) {
-            const int row = x0 + R * (j * TEAMS + tm);
-            tma_store_1d(yp + (int64_t)row * NY, ost + slot * TEAMS * NY + tm * NY, NY * 8, pol_out);
-          }
+        team_sync<M>(team);
+        if (elected) {
+          const int row = x0 + R * x1;
+          tma_store_1d(yp + (int64_t)row * NY, ostt + slot * NY, NY * 8, pol);
           bulk_commit();
         }
       }
     }
   }
-  if (tid == 0) bulk_wait_all();
+  if (elected) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- dispatch
 template <class G>
 constexpr size_t fwd_smem(int S) {
-  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * G::TS + G::KX * G::KY + G::NY + G::DX) +
-         8 * S + 64;
+  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * G::TS +
+                           G::TEAMS * 8 * (G::A * (G::T + 2) + 8) + G::KX * G::KY + G::NY + G::DX) +
+         16 * S + 64;
 }
 template <class G>
 constexpr size_t inv_smem(int SO) {
-  return sizeof(float2) * (3 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS + (size_t)SO * G::TEAMS * G::NY +
+  return sizeof(float2) * (2 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS + (size_t)SO * G::TEAMS * G::NY +
                            G::NY + G::DX) +
          16 + 64;
 }
@@ -439,7 +480,7 @@ static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w,
     if (e != cudaSuccess) return e;
     int64_t planes = B * H;
     int grid = (int)(planes < sms ? planes : sms);
-    plane_fwd2d_kernel<G, S><<<grid, G::NTH, smem, st>>>(x, A, planes, tw);
+    plane_fwd2d_kernel<G, S><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
     ++g_launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (mark) mark(st);

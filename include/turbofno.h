@@ -99,6 +99,17 @@ size_t tfno_workspace_bytes(const tfno_cfg* cfg, int mode, int prec);
 int tfno_layer_forward(const tfno_cfg* cfg, int mode, int prec, const void* x, const void* w, void* y,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Spectrum-level entry points (building blocks of the hidden-dim split and
+ * of layer chains).  modes are natural-order [planes][keep_x][keep_y] c64.
+ *   forward: modes[B][H] = first-keep 2D (rank 2) / 1D (rank 1) DFT of x[B][H]
+ *   inverse: y[B][N] = scale * zero-padded inverse (1/(dx*dy) normalised) of modes[B][N]
+ * Workspace: tfno_spectrum_workspace_bytes(cfg, -1 forward / +1 inverse). */
+size_t tfno_spectrum_workspace_bytes(const tfno_cfg* cfg, int direction);
+int tfno_spectrum_forward(const tfno_cfg* cfg, const void* x, void* modes, void* workspace, size_t workspace_bytes,
+                          void* stream);
+int tfno_spectrum_inverse(const tfno_cfg* cfg, const void* modes, void* y, float scale, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* Batched pencils FFT: pencil p (p < P) of `in` starts at (p / in_P0) * in_s1 + (p % in_P0) * in_s0
  * and element e is at start + e * in_es (complex elements); same for `out`.
  * Reads src_len elements, writes keep elements; direction -1 forward, +1 inverse (x 1/n). */

@@ -48,6 +48,10 @@ _SIGS = {
                                         _I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
     "tfno_cgemm": (ctypes.c_int, [_I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _VP, _I64, _I64, _I64,
                                   _VP, _I64, _I64, _I64, ctypes.c_float, _VP]),
+    "tfno_spectrum_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(TfnoCfg), ctypes.c_int]),
+    "tfno_spectrum_forward": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "tfno_spectrum_inverse": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), _VP, _VP, ctypes.c_float, _VP,
+                                             ctypes.c_size_t, _VP]),
     "tfno_launch_count": (ctypes.c_longlong, []),
     "tfno_set_stage_events": (None, [_VP, ctypes.c_int]),
     "tfno_layer_schedule": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int,

@@ -429,6 +429,67 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
   return cuda_status(launch_cgemm(g, (cudaStream_t)stream));
 }
 
+size_t tfno_spectrum_workspace_bytes(const tfno_cfg* c, int direction) {
+  if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
+  if (c->rank != 2 || plane2d_supported(c)) return 0;
+  Geo g = geo_of(c);
+  return (size_t)((direction < 0 ? g.H : g.N) * g.B * g.kx * g.dy) * sizeof(float2);
+}
+
+int tfno_spectrum_forward(const tfno_cfg* c, const void* xv, void* modes, void* wsv, size_t ws_bytes, void* stream) {
+  if (!c || tfno_config_violations(c, nullptr, 8) || !xv || !modes) return TFNO_EINVAL;
+  if (c->dim_x > TFNO_TW_MAX || c->dim_y > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
+  if (ws_bytes < tfno_spectrum_workspace_bytes(c, -1)) return TFNO_EWORKSPACE;
+  int err = 0;
+  const float2* tw = twiddle_table(err);
+  if (err) return err;
+  cudaStream_t st = (cudaStream_t)stream;
+  Geo g = geo_of(c);
+  const float2* x = (const float2*)xv;
+  float2* A = (float2*)modes;
+  if (plane2d_supported(c)) return cuda_status(launch_plane2d_fwd(c, x, A, tw, st));
+  const float2* src = x;
+  if (g.rank == 2) {
+    float2* s1 = (float2*)wsv;
+    FftPencilArgs a = pencil_args((int)g.dx, (int)g.kx, (int)g.dx, g.B * g.H * g.dy, x,
+                                  PencilMap{g.dy, g.dx * g.dy, 1, g.dy}, s1, PencilMap{g.dy, g.kx * g.dy, 1, g.dy},
+                                  1.0f, tw);
+    if (launch_fft_pencils(a, -1, st) != cudaSuccess) return TFNO_ECUDA;
+    src = s1;
+  }
+  FftPencilArgs a = pencil_args((int)g.dy, (int)g.ky, (int)g.dy, g.B * g.H * g.kx, src, PencilMap{1, g.dy, 0, 1}, A,
+                                PencilMap{1, g.ky, 0, 1}, 1.0f, tw);
+  return cuda_status(launch_fft_pencils(a, -1, st));
+}
+
+int tfno_spectrum_inverse(const tfno_cfg* c, const void* modes, void* yv, float scale, void* wsv, size_t ws_bytes,
+                          void* stream) {
+  if (!c || tfno_config_violations(c, nullptr, 8) || !yv || !modes) return TFNO_EINVAL;
+  if (c->dim_x > TFNO_TW_MAX || c->dim_y > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
+  if (ws_bytes < tfno_spectrum_workspace_bytes(c, 1)) return TFNO_EWORKSPACE;
+  int err = 0;
+  const float2* tw = twiddle_table(err);
+  if (err) return err;
+  cudaStream_t st = (cudaStream_t)stream;
+  Geo g = geo_of(c);
+  const float2* Cm = (const float2*)modes;
+  float2* y = (float2*)yv;
+  if (plane2d_supported(c))
+    return cuda_status(launch_plane2d_inv(c, Cm, y, (float)(scale / ((double)g.dx * g.dy)), tw, st));
+  float2* dst = g.rank == 2 ? (float2*)wsv : y;
+  float sy = (float)(1.0 / (double)g.dy) * (g.rank == 2 ? 1.0f : scale);
+  FftPencilArgs a = pencil_args((int)g.dy, (int)g.dy, (int)g.ky, g.B * g.N * g.kx, Cm, PencilMap{1, g.ky, 0, 1}, dst,
+                                PencilMap{1, g.dy, 0, 1}, sy, tw);
+  if (launch_fft_pencils(a, 1, st) != cudaSuccess) return TFNO_ECUDA;
+  if (g.rank == 2) {
+    FftPencilArgs b = pencil_args((int)g.dx, (int)g.dx, (int)g.kx, g.B * g.N * g.dy, dst,
+                                  PencilMap{g.dy, g.kx * g.dy, 1, g.dy}, y, PencilMap{g.dy, g.dx * g.dy, 1, g.dy},
+                                  (float)(scale / (double)g.dx), tw);
+    if (launch_fft_pencils(b, 1, st) != cudaSuccess) return TFNO_ECUDA;
+  }
+  return TFNO_OK;
+}
+
 int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv, void* yv,
                        void* wsv, size_t ws_bytes, void* stream) {
   if (!c || mode < TFNO_STAGED || mode > TFNO_FULLY_FUSED) return TFNO_EINVAL;

@@ -142,7 +142,7 @@ constexpr int kComputeBar = 15;
 // Warp-specialised: warp NTH/32 is the TMA producer (ring of S slots, full /
 // empty mbarriers); the NTH compute threads form row teams that synchronise
 // only inside the team, plus one compute-wide barrier per class (column pass).
-template <class G, int S>
+template <class G, int S, bool NATURAL>
 __global__ void __launch_bounds__(G::NTH + 32, 1)
     plane_fwd2d_kernel(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes,
                        const float2* __restrict__ twg) {
@@ -303,9 +303,10 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
           const int tau = tid + jj * NTH;
           if (tau < 8 * KY) {
             const int q = tau % KY, s2 = tau / KY;
+            const int qo = NATURAL ? (q / T) + 8 * (q % T) : q;
 #pragma unroll
             for (int u = 0; u < KA; ++u) {
-              dst[(s2 + 8 * u) * KY + q] = acc[jj][u];
+              dst[(s2 + 8 * u) * KY + qo] = acc[jj][u];
               acc[jj][u] = make_float2(0.f, 0.f);
             }
           }
@@ -318,10 +319,10 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
 // ============================================================== inverse
 // Row teams run decoupled (team barriers only); each team's elected thread
 // TMA-stores its own finished rows from a per-team staging ring.
-template <class G, int SO>
+template <class G, int SO, bool NATURAL>
 __global__ void __launch_bounds__(G::NTH, 1)
     plane_inv2d_kernel(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes,
-                       const float2* __restrict__ twg) {
+                       const float2* __restrict__ twg, float scale) {
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
   const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
   for (int k = tid; k < NY; k += NTH) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]));
-  for (int k = tid; k < DX; k += NTH) twx[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]));
+  for (int k = tid; k < DX; k += NTH) twx[k] = cscale(conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)])), scale);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -373,13 +374,14 @@ __global__ void __launch_bounds__(G::NTH, 1)
         const int q = tau % KY, s2 = tau / KY;
         float2 w[KA];
 #pragma unroll
+        const int qi = NATURAL ? (q / T) + 8 * (q % T) : q;
         for (int u = 0; u < KA; ++u) {
           const int p = s2 + 8 * u;
-          w[u] = cmul(cin[p * KY + q], twx[p * x0]);
+          w[u] = cmul(cin[p * KY + qi], twx[p * x0]);  // twx carries the output scale
         }
         dft_small<KA, 1>(w);
 #pragma unroll
-        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twx[s2 * i * R]);
+        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twy[s2 * i * (NY / KX)]);
 #pragma unroll
         for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KY + q] = w[i];
       }
@@ -467,46 +469,64 @@ static int num_sms() {
   return n;
 }
 
+template <class G, int S>
+static cudaError_t launch_fwd(const float2* x, float2* A, int64_t planes, const float2* tw, bool natural,
+                              cudaStream_t st) {
+  const int sms = num_sms();
+  size_t smem = fwd_smem<G>(S);
+  int grid = (int)(planes < sms ? planes : sms);
+  if (grid < 1) return cudaSuccess;
+  cudaError_t e;
+  if (natural) {
+    e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    plane_fwd2d_kernel<G, S, true><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
+  } else {
+    e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    plane_fwd2d_kernel<G, S, false><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <class G, int SO>
+static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale, bool natural,
+                              cudaStream_t st) {
+  const int sms = num_sms();
+  size_t smem = inv_smem<G>(SO);
+  int grid = (int)(planes < sms ? planes : sms);
+  if (grid < 1) return cudaSuccess;
+  cudaError_t e;
+  if (natural) {
+    e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    plane_inv2d_kernel<G, SO, true><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
+  } else {
+    e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    plane_inv2d_kernel<G, SO, false><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 template <class G, int S, int SO>
 static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
                             const float2* tw, cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
-  const int sms = num_sms();
-  // forward planes
-  {
-    size_t smem = fwd_smem<G>(S);
-    cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    int64_t planes = B * H;
-    int grid = (int)(planes < sms ? planes : sms);
-    plane_fwd2d_kernel<G, S><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
-    ++g_launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (mark) mark(st);
-  }
+  cudaError_t e = launch_fwd<G, S>(x, A, B * H, tw, false, st);
+  if (e != cudaSuccess) return e;
+  if (mark) mark(st);
   // channel mixing over modes, 1/(dx*dy) folded into alpha
-  {
-    const int64_t MQ = (int64_t)G::KX * G::KY;
-    GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ,
-                (float)(1.0 / ((double)G::DX * G::NY))};
-    cudaError_t e = launch_cgemm(ga, st);
-    if (e != cudaSuccess) return e;
-    if (mark) mark(st);
-  }
-  // inverse planes
-  {
-    size_t smem = inv_smem<G>(SO);
-    cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    int64_t planes = B * N;
-    int grid = (int)(planes < sms ? planes : sms);
-    plane_inv2d_kernel<G, SO><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw);
-    ++g_launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (mark) mark(st);
-  }
+  const int64_t MQ = (int64_t)G::KX * G::KY;
+  GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ, (float)(1.0 / ((double)G::DX * G::NY))};
+  if ((e = launch_cgemm(ga, st)) != cudaSuccess) return e;
+  if (mark) mark(st);
+  if ((e = launch_inv<G, SO>(Cm, y, B * N, tw, 1.0f, false, st)) != cudaSuccess) return e;
+  if (mark) mark(st);
   return cudaSuccess;
 }
 
@@ -523,6 +543,28 @@ bool plane2d_supported(const tfno_cfg* c) {
   const int dx = c->dim_x, dy = c->dim_y, kx = c->keep_x, ky = c->keep_y;
   return (dx == 512 && dy == 512 && kx == 64 && ky == 64) || (dx == 256 && dy == 256 && kx == 32 && ky == 32) ||
          (dx == 256 && dy == 256 && kx == 16 && ky == 16) || (dx == 128 && dy == 128 && kx == 16 && ky == 16);
+}
+
+cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw,
+                               cudaStream_t st) {
+  const int dx = c->dim_x, kx = c->keep_x;
+  const int64_t P = (int64_t)c->batch * c->hidden_dim;
+  if (dx == 512) return launch_fwd<G512, 3>(x, modes, P, tw, true, st);
+  if (dx == 256 && kx == 32) return launch_fwd<G256a, 4>(x, modes, P, tw, true, st);
+  if (dx == 256 && kx == 16) return launch_fwd<G256b, 4>(x, modes, P, tw, true, st);
+  if (dx == 128) return launch_fwd<G128, 4>(x, modes, P, tw, true, st);
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y, float scale, const float2* tw,
+                               cudaStream_t st) {
+  const int dx = c->dim_x, kx = c->keep_x;
+  const int64_t P = (int64_t)c->batch * c->output_dim;
+  if (dx == 512) return launch_inv<G512, 2>(modes, y, P, tw, scale, true, st);
+  if (dx == 256 && kx == 32) return launch_inv<G256a, 2>(modes, y, P, tw, scale, true, st);
+  if (dx == 256 && kx == 16) return launch_inv<G256b, 2>(modes, y, P, tw, scale, true, st);
+  if (dx == 128) return launch_inv<G128, 2>(modes, y, P, tw, scale, true, st);
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,

@@ -1,0 +1,74 @@
+"""GPU (single device): the per-rank compute of the multi-GPU drivers.
+Batch shards are bitwise equal to the unsharded run (batch elements are
+independent); hidden-split partials summed over ranks equal the full layer;
+the spectrum-level entry points match the oracle."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2504_11681_b200 as T
+    from oracle import fnofuse_port as O
+    from paper_2504_11681_b200 import multigpu as MG
+    return T, O, MG, torch
+
+
+@pytest.mark.parametrize("shape", [(6, 8, 8, 256, 256, 32, 32, 2), (5, 16, 12, 1, 256, 1, 32, 1),
+                                   (4, 6, 5, 32, 64, 8, 16, 2)])
+def test_batch_shards_bitwise_equal_unsharded(env, shape):
+    T, O, MG, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = O.random_inputs(cfg, 3)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    full = T.run_layer_device(cfg, xd, wd)
+    for world in (2, 3):
+        parts = []
+        for r in range(world):
+            sh = MG.BatchSharded(cfg, world, r)
+            b0, b1 = sh.bounds
+            parts.append(sh.forward(xd[b0:b1].contiguous(), wd))
+        assert torch.equal(torch.cat(parts), full)
+
+
+@pytest.mark.parametrize("shape", [(2, 16, 8, 256, 256, 32, 32, 2), (3, 12, 6, 32, 64, 8, 16, 2),
+                                   (3, 10, 4, 1, 128, 1, 32, 1)])
+def test_hidden_split_partials_sum_to_layer(env, shape):
+    T, O, MG, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = O.random_inputs(cfg, 4)
+    ref = O.run_layer_values(cfg, x, w)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    world = 2
+    C = None
+    for r in range(world):
+        h0, h1 = MG.shard_bounds(cfg.hidden_dim, world, r)
+        part = MG.hidden_split_partial(cfg, xd[:, h0:h1].contiguous(), wd[h0:h1])
+        C = part if C is None else C + part       # what all_reduce(SUM) computes over NVLink
+    oc = T.FnoLayerConfig(cfg.batch, 1, cfg.output_dim, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
+    y = MG.spectrum_inverse(oc, C, (cfg.batch, cfg.output_dim))
+    assert T.max_rel_error(y.cpu().numpy(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 3, 512, 512, 64, 64, 2), (2, 3, 3, 64, 32, 8, 4, 2), (3, 2, 2, 1, 64, 1, 8, 1)])
+def test_spectrum_entry_points_vs_oracle(env, shape):
+    T, O, MG, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x, _ = O.random_inputs(cfg, 5)
+    modes = MG.spectrum_forward(cfg, torch.from_numpy(x).cuda())
+    want = O.dft_oracle(x) if cfg.rank == 1 else None
+    t = x.astype(np.complex128)
+    if cfg.rank == 2:
+        t = np.einsum("jx,bhxy->bhjy", O.dft_matrix(cfg.dim_x), t)[:, :, :cfg.keep_x, :]
+    want = np.einsum("jy,bhxy->bhxj", O.dft_matrix(cfg.dim_y), t)[..., :cfg.keep_y]
+    assert T.max_rel_error(modes.cpu().numpy(), want) < 1e-5
+    oc = T.FnoLayerConfig(cfg.batch, 1, cfg.hidden_dim, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
+    y = MG.spectrum_inverse(oc, modes, (cfg.batch, cfg.hidden_dim), scale=2.0)
+    spec = np.zeros(x.shape, np.complex128)
+    spec[:, :, :cfg.keep_x, :cfg.keep_y] = want
+    yr = 2.0 * np.fft.ifft2(spec, axes=(2, 3))
+    assert T.max_rel_error(y.cpu().numpy(), yr) < 1e-5

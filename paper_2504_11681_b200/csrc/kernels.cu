@@ -165,9 +165,122 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
   }
 }
 
+// Mode-layout fast path: A[b][k][m] and C[b][n][m] m-contiguous, W[k][n]
+// n-contiguous.  CTA tile 64 (m) x 128 (n) so the A panel is streamed from
+// HBM once for N <= 128; BK = 16; 4 x 8 complex accumulators per thread
+// (m = tm + 16 i, n = tn + 16 j: conflict-free / broadcast shared reads);
+// next chunk prefetched into registers (float4) while the current one is
+// consumed from shared memory (double buffer).
+template <int TI, int TJ>
+__global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
+  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = 16;
+  __shared__ __align__(16) float2 As[2][FBK][FBM];
+  __shared__ __align__(16) float2 Ws[2][FBK][FBN];
+  const int tid = threadIdx.x;
+  const int tm = tid % 16, tn = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
+  const int64_t b = blockIdx.z;
+  const float2* __restrict__ A = g.A + b * g.a_bs;
+  const float2* __restrict__ W = g.W + b * g.w_bs;
+  // loader mapping: A chunk = FBK x FBM complex = 512 float4 (2 / thread),
+  //                 W chunk = FBK x FBN complex = 1024 float4 (4 / thread)
+  constexpr int NA = FBK * FBM / 2 / 256, NW = FBK * FBN / 2 / 256;  // float4 per thread
+  float4 ra[NA], rw[NW];
+  auto load_chunk = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
+      const int64_t gk = k0 + kk, gm = m0 + mm;
+      if (gk < g.K && gm + 1 < g.M) {
+        ra[r] = __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + gm));
+      } else {
+        float2 v0 = (gk < g.K && gm < g.M) ? A[gk * g.a_ks + gm] : make_float2(0.f, 0.f);
+        ra[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBN / 2), nn = (i % (FBN / 2)) * 2;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      if (gk < g.K && gn + 1 < g.N) {
+        rw[r] = __ldg(reinterpret_cast<const float4*>(W + gk * g.w_ks + gn));
+      } else {
+        float2 v0 = (gk < g.K && gn < g.N) ? W[gk * g.w_ks + gn] : make_float2(0.f, 0.f);
+        rw[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
+      }
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int i = tid + r * 256;
+      *reinterpret_cast<float4*>(&As[buf][i / (FBM / 2)][(i % (FBM / 2)) * 2]) = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int i = tid + r * 256;
+      *reinterpret_cast<float4*>(&Ws[buf][i / (FBN / 2)][(i % (FBN / 2)) * 2]) = rw[r];
+    }
+  };
+  float2 acc[TI][TJ];
+#pragma unroll
+  for (int i = 0; i < TI; ++i)
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += FBK) {
+    const bool more = k0 + FBK < g.K;
+    if (more) load_chunk(k0 + FBK);
+#pragma unroll
+    for (int kk = 0; kk < FBK; ++kk) {
+      float2 av[TI], bv[TJ];
+#pragma unroll
+      for (int i = 0; i < TI; ++i) av[i] = As[buf][kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) bv[j] = Ws[buf][kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+    }
+    if (more) {
+      store_chunk(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  float2* C = g.C + b * g.c_bs;
+#pragma unroll
+  for (int j = 0; j < TJ; ++j) {
+    const int64_t gn = n0 + tn + 16 * j;
+    if (gn >= g.N) continue;
+#pragma unroll
+    for (int i = 0; i < TI; ++i) {
+      const int64_t gm = m0 + tm + 16 * i;
+      if (gm < g.M) C[gn * g.c_ns + gm] = cscale(acc[i][j], g.alpha);
+    }
+  }
+}
+
 cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
-  dim3 grid((unsigned)((g.M + GBM - 1) / GBM), (unsigned)((g.N + GBN - 1) / GBN), (unsigned)g.batch);
-  cgemm_kernel<<<grid, 256, 0, s>>>(g);
+  const bool fast = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) &&
+                    (g.w_ks % 2 == 0) && (g.w_bs % 2 == 0) && g.N > 16 && g.M >= 64 &&
+                    ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0);
+  if (fast && g.N > 64) {
+    dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
+    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);
+  } else if (fast && g.M >= 128) {
+    dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
+    cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(g);
+  } else {
+    dim3 grid((unsigned)((g.M + GBM - 1) / GBM), (unsigned)((g.N + GBN - 1) / GBN), (unsigned)g.batch);
+    cgemm_kernel<<<grid, 256, 0, s>>>(g);
+  }
   ++g_launches;
   return cudaGetLastError();
 }

@@ -107,7 +107,9 @@ struct PlaneGeo {
   static constexpr int KA = KX / 8;      // kx = 8 * KA
   static constexpr int IPC = KX / TEAMS; // iterations per class
   static constexpr int PAD = ((-7 * A) % 16 + 16) % 16;
-  static constexpr int TS = M + PAD;     // transposed-row stride
+  static constexpr int RT = T + 2;                 // reduction buffer: padded t-stride
+  static constexpr int RS = A * RT + 8;            //                   per-r stride
+  static constexpr int TS = M + PAD;  // transposed-row stride (== A mod 16: conflict-free reads)
   static constexpr int TASKS2 = (8 * KY + NTH - 1) / NTH;
   static_assert(A >= 1 && (1 << LOGA) == A, "A power of two");
   static_assert((1 << LOGT) == T && T <= A && T <= 8, "ky <= 8*min(8, dy/64)");
@@ -148,8 +150,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
                        const float2* __restrict__ twg) {
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
-  constexpr int RT = T + 2;               // padded t-stride of the reduction buffer
-  constexpr int RS = A * RT + 8;          // per-r stride (bank-conflict-free 16B stores / 8B loads)
+  constexpr int RT = G::RT, RS = G::RS;
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);
   float2* tr = ring + S * TEAMS * NY;
@@ -447,8 +448,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
 // ---------------------------------------------------------------- dispatch
 template <class G>
 constexpr size_t fwd_smem(int S) {
-  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * G::TS +
-                           G::TEAMS * 8 * (G::A * (G::T + 2) + 8) + G::KX * G::KY + G::NY + G::DX) +
+  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * (G::TS + G::RS) + G::KX * G::KY +
+                           G::NY + G::DX) +
          16 * S + 64;
 }
 template <class G>
@@ -536,7 +537,7 @@ using G256b = PlaneGeo<256, 16, 256, 16, 512>;
 using G128 = PlaneGeo<128, 16, 128, 16, 256>;
 
 static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
-static_assert(inv_smem<G512>(2) <= 227 * 1024, "smem");
+static_assert(inv_smem<G512>(3) <= 227 * 1024, "smem");
 
 bool plane2d_supported(const tfno_cfg* c) {
   if (c->rank != 2 || c->batch * (int64_t)c->hidden_dim > (1LL << 40)) return false;
@@ -560,7 +561,7 @@ cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y
                                cudaStream_t st) {
   const int dx = c->dim_x, kx = c->keep_x;
   const int64_t P = (int64_t)c->batch * c->output_dim;
-  if (dx == 512) return launch_inv<G512, 2>(modes, y, P, tw, scale, true, st);
+  if (dx == 512) return launch_inv<G512, 3>(modes, y, P, tw, scale, true, st);
   if (dx == 256 && kx == 32) return launch_inv<G256a, 2>(modes, y, P, tw, scale, true, st);
   if (dx == 256 && kx == 16) return launch_inv<G256b, 2>(modes, y, P, tw, scale, true, st);
   if (dx == 128) return launch_inv<G128, 2>(modes, y, P, tw, scale, true, st);
@@ -572,7 +573,7 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
                                  void (*mark)(cudaStream_t)) {
   (void)prec;
   const int dx = c->dim_x, kx = c->keep_x;
-  if (dx == 512) return run_pair<G512, 3, 2>(c, x, w, y, A, Cm, tw, st, mark);
+  if (dx == 512) return run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, st, mark);
   if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);
   if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);
   if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, st, mark);

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "plane2d.cuh"
+#include "rows1d.cuh"
 
 using namespace tfno;
 
@@ -122,9 +123,31 @@ bool fused_tiling(int n, int keep, int N, FusedArgs& a) {
   return fused_smem_bytes(a) <= 220 * 1024;
 }
 
+// compile-time row kernels (rows1d.cu): C tile [keep x NT] in registers of 512 threads
+bool rows_tiling(int n, int keep, int N, int& NT) {
+  if (!rows_supported(n) || keep > 2048) return false;
+  const int MT = (keep + 3) / 4;
+  const int ntg_max = 512 / MT;
+  if (ntg_max < 1) return false;
+  NT = ((N + 3) / 4) * 4;
+  if (NT > 4 * ntg_max) NT = 4 * ntg_max;
+  while (rows_fused_smem_bytes(n, keep, NT) > 220 * 1024 && NT > 4) NT -= 4;
+  return rows_fused_smem_bytes(n, keep, NT) <= 220 * 1024;
+}
+
+// FFT over pencils: contiguous rows of a specialised length go to the
+// compile-time row kernel, everything else to the general pencil kernel
+cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st) {
+  const bool rows = a.im.P0 == 1 && a.im.s0 == 0 && a.im.es == 1 && a.om.P0 == 1 && a.om.s0 == 0 && a.om.es == 1;
+  if (rows && rows_supported(a.n))
+    return launch_rows_fft(a.n, dir, a.in, a.im.s1, a.out, a.om.s1, a.P, a.keep, a.src_len, a.scale, a.twg, st);
+  return launch_fft_pencils(a, dir, st);
+}
+
 // schedule decision shared by workspace sizing and the forward
 struct Sched {
-  bool staged = false, plane2d = false;
+  bool staged = false, plane2d = false, rows_fast = false;
+  int rows_NT = 0;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
   int launches = 0;
@@ -150,7 +173,17 @@ Sched make_sched(const tfno_cfg* c, int mode) {
     return s;
   }
   FusedArgs fa{};
-  bool ok = fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+  int NT = 0;
+  bool ok;
+  if (rows_tiling((int)g.dy, (int)g.ky, (int)g.N, NT)) {
+    // fused only while the C tile covers >= half of N (else the FFT would be
+    // recomputed per n-tile): otherwise the unfused schedule of fast kernels
+    ok = (g.N + NT - 1) / NT <= 2;
+    s.rows_fast = ok;
+    s.rows_NT = NT;
+  } else {
+    ok = fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+  }
   s.fg = want_fg && ok;
   s.gi = want_gi && ok;
   s.need_s1 = s.need_mid = (g.rank == 2);
@@ -415,7 +448,7 @@ int tfno_fft_execute(int n, int direction, int keep, int src_len, int64_t P, con
   FftPencilArgs a = pencil_args(n, keep, src_len, P, (const float2*)in, PencilMap{in_P0, in_s1, in_s0, in_es},
                                 (float2*)out, PencilMap{out_P0, out_s1, out_s0, out_es},
                                 direction < 0 ? 1.0f : (float)(1.0 / n), tw);
-  return cuda_status(launch_fft_pencils(a, direction < 0 ? -1 : 1, (cudaStream_t)stream));
+  return cuda_status(launch_pencils_auto(a, direction < 0 ? -1 : 1, (cudaStream_t)stream));
 }
 
 int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,
@@ -454,12 +487,12 @@ int tfno_spectrum_forward(const tfno_cfg* c, const void* xv, void* modes, void* 
     FftPencilArgs a = pencil_args((int)g.dx, (int)g.kx, (int)g.dx, g.B * g.H * g.dy, x,
                                   PencilMap{g.dy, g.dx * g.dy, 1, g.dy}, s1, PencilMap{g.dy, g.kx * g.dy, 1, g.dy},
                                   1.0f, tw);
-    if (launch_fft_pencils(a, -1, st) != cudaSuccess) return TFNO_ECUDA;
+    if (launch_pencils_auto(a, -1, st) != cudaSuccess) return TFNO_ECUDA;
     src = s1;
   }
   FftPencilArgs a = pencil_args((int)g.dy, (int)g.ky, (int)g.dy, g.B * g.H * g.kx, src, PencilMap{1, g.dy, 0, 1}, A,
                                 PencilMap{1, g.ky, 0, 1}, 1.0f, tw);
-  return cuda_status(launch_fft_pencils(a, -1, st));
+  return cuda_status(launch_pencils_auto(a, -1, st));
 }
 
 int tfno_spectrum_inverse(const tfno_cfg* c, const void* modes, void* yv, float scale, void* wsv, size_t ws_bytes,
@@ -480,12 +513,12 @@ int tfno_spectrum_inverse(const tfno_cfg* c, const void* modes, void* yv, float 
   float sy = (float)(1.0 / (double)g.dy) * (g.rank == 2 ? 1.0f : scale);
   FftPencilArgs a = pencil_args((int)g.dy, (int)g.dy, (int)g.ky, g.B * g.N * g.kx, Cm, PencilMap{1, g.ky, 0, 1}, dst,
                                 PencilMap{1, g.dy, 0, 1}, sy, tw);
-  if (launch_fft_pencils(a, 1, st) != cudaSuccess) return TFNO_ECUDA;
+  if (launch_pencils_auto(a, 1, st) != cudaSuccess) return TFNO_ECUDA;
   if (g.rank == 2) {
     FftPencilArgs b = pencil_args((int)g.dx, (int)g.dx, (int)g.kx, g.B * g.N * g.dy, dst,
                                   PencilMap{g.dy, g.kx * g.dy, 1, g.dy}, y, PencilMap{g.dy, g.dx * g.dy, 1, g.dy},
                                   (float)(scale / (double)g.dx), tw);
-    if (launch_fft_pencils(b, 1, st) != cudaSuccess) return TFNO_ECUDA;
+    if (launch_pencils_auto(b, 1, st) != cudaSuccess) return TFNO_ECUDA;
   }
   return TFNO_OK;
 }
@@ -532,7 +565,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     FftPencilArgs a = pencil_args((int)g.dx, (int)g.kx, (int)g.dx, g.B * g.H * g.dy, x,
                                   PencilMap{g.dy, g.dx * g.dy, 1, g.dy}, s1, PencilMap{g.dy, g.kx * g.dy, 1, g.dy},
                                   1.0f, tw);
-    if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+    if ((e = launch_pencils_auto(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
     src = s1;
   }
@@ -542,12 +575,21 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     // y-FFT of every source row -> A[B,H,kx,ky]
     FftPencilArgs a = pencil_args((int)g.dy, (int)g.ky, (int)g.dy, rows_in, src, PencilMap{1, g.dy, 0, 1}, A,
                                   PencilMap{1, g.ky, 0, 1}, 1.0f, tw);
-    if ((e = launch_fft_pencils(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
+    if ((e = launch_pencils_auto(a, -1, st)) != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   }
   if (s.fg || s.gi) {
     FusedArgs fa{};
-    fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+    if (s.rows_fast) {
+      fa.n = (int)g.dy;
+      fa.keep = (int)g.ky;
+      fa.N = (int)g.N;
+      fa.NT = s.rows_NT;
+      fa.KC = rows_chunk((int)g.dy);
+      fa.EC = fa.KC;
+    } else {
+      fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
+    }
     fa.H = (int)g.H;
     fa.gx = (int)g.kx;
     fa.G = g.B * g.kx;
@@ -571,7 +613,8 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     fa.twg = tw;
     fa.inv_scale = (float)(1.0 / (double)g.dy);
     if (fa.G > 2147483647LL || (g.N + fa.NT - 1) / fa.NT > 65535) return TFNO_EUNSUPPORTED;
-    if ((e = launch_fused(fa, s.fg, s.gi, st)) != cudaSuccess) return TFNO_ECUDA;
+    e = s.rows_fast ? launch_rows_fused(fa, s.fg, s.gi, st) : launch_fused(fa, s.fg, s.gi, st);
+    if (e != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   } else {
     // C[b, n, pq] = sum_h A[b, h, pq] W[h, n]
@@ -584,14 +627,14 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   if (!s.gi) {
     FftPencilArgs a = pencil_args((int)g.dy, (int)g.dy, (int)g.ky, rows_out, Cm, PencilMap{1, g.ky, 0, 1}, dst_mid,
                                   PencilMap{1, g.dy, 0, 1}, (float)(1.0 / (double)g.dy), tw);
-    if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+    if ((e = launch_pencils_auto(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   }
   if (g.rank == 2) {
     FftPencilArgs a = pencil_args((int)g.dx, (int)g.dx, (int)g.kx, g.B * g.N * g.dy, mid,
                                   PencilMap{g.dy, g.kx * g.dy, 1, g.dy}, y, PencilMap{g.dy, g.dx * g.dy, 1, g.dy},
                                   (float)(1.0 / (double)g.dx), tw);
-    if ((e = launch_fft_pencils(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
+    if ((e = launch_pencils_auto(a, 1, st)) != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   }
   return TFNO_OK;

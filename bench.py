@@ -322,7 +322,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "us_per_layer": round(ms * 1e3, 2),
         "layers_per_s": round(ws * 1e3 / ms, 2), "higher_is_better": True,
         "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None,
-        "dtype": "fp32 (complex64 in/out, fp32 arithmetic)" if prec == "fp32" else f"{prec} contraction",
+        "dtype": ("fp32 (complex64 in/out, fp32 arithmetic)" if prec == "fp32" else
+                  f"fp32 FFTs + {prec} tcgen05 channel contraction (complex64 in/out)"),
         "data": "synthetic (device-generated N(0,1) re/im, seeded per rank)",
         "config": {"workload": desc, "batch_per_gpu": B, "global_batch": B * ws, "hidden": H, "out": N,
                    "dims": [dx, dy], "keep": [kx, ky], "rank": rk, "mode": mode, "precision": prec,
@@ -469,7 +470,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="fully_fused")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "bf16"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "tf32x3"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true")

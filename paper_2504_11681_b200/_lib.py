@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libturbofno.so")
 
 MODE_CODES = {"staged": 0, "fft_optimized": 1, "fused_fft_gemm": 2,
               "fused_gemm_ifft": 3, "fully_fused": 4}
-PREC_CODES = {"fp32": 0, "tf32": 1, "bf16": 2}
+PREC_CODES = {"fp32": 0, "tf32": 1, "bf16": 2, "tf32x3": 3}
 VIOLATION_BITS = {1: "InvalidRankShape", 2: "NonPowerOfTwoLength", 4: "TruncationExceedsLength",
                   8: "TileDivisibilityViolation", 16: "BatchSizeMismatch"}
 
@@ -52,6 +52,8 @@ _SIGS = {
     "tfno_spectrum_forward": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), _VP, _VP, _VP, ctypes.c_size_t, _VP]),
     "tfno_spectrum_inverse": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), _VP, _VP, ctypes.c_float, _VP,
                                              ctypes.c_size_t, _VP]),
+    "tfno_cgemm_prec": (ctypes.c_int, [_I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _VP, _I64, _I64, _I64,
+                                       _VP, _I64, _I64, _I64, ctypes.c_float, ctypes.c_int, _VP]),
     "tfno_launch_count": (ctypes.c_longlong, []),
     "tfno_set_stage_events": (None, [_VP, ctypes.c_int]),
     "tfno_layer_schedule": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int,

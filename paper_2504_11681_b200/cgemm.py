@@ -78,9 +78,11 @@ def _check_shapes(p: GemmProblem, a: ComplexMatrix, b: ComplexMatrix) -> None:
         raise ShapeMismatch("; ".join(str(v) for v in bad))
 
 
-def cgemm_device(a, b, out=None, alpha: float = 1.0):
+def cgemm_device(a, b, out=None, alpha: float = 1.0, precision: str = "fp32"):
     """Device API: C = alpha * a @ b for CUDA complex64 tensors of any
-    strides (2-D, or 3-D batched along dim 0)."""
+    strides (2-D, or 3-D batched along dim 0).  precision "tf32" / "tf32x3"
+    runs the tcgen05 tensor-core contraction (mode layout required: a and the
+    output m-contiguous, b row-major with N <= 128)."""
     t = _device.torch()
     batched = a.dim() == 3
     A = a if batched else a.unsqueeze(0)
@@ -93,11 +95,12 @@ def cgemm_device(a, b, out=None, alpha: float = 1.0):
         out = t.empty((bsz, N, M), dtype=t.complex64, device=a.device).transpose(1, 2)
     C = out if out.dim() == 3 else out.unsqueeze(0)
     w_bs = Bm.stride(0) if Bm.shape[0] > 1 else 0
-    rc = lib().tfno_cgemm(M, N, K, bsz, A.data_ptr(), A.stride(1), A.stride(2), A.stride(0),
-                          Bm.data_ptr(), Bm.stride(1), Bm.stride(2), w_bs,
-                          C.data_ptr(), C.stride(1), C.stride(2), C.stride(0), float(alpha),
-                          _device.stream_ptr())
-    check(rc, "tfno_cgemm")
+    from ._lib import PREC_CODES
+    rc = lib().tfno_cgemm_prec(M, N, K, bsz, A.data_ptr(), A.stride(1), A.stride(2), A.stride(0),
+                               Bm.data_ptr(), Bm.stride(1), Bm.stride(2), w_bs,
+                               C.data_ptr(), C.stride(1), C.stride(2), C.stride(0), float(alpha),
+                               PREC_CODES[precision], _device.stream_ptr())
+    check(rc, "tfno_cgemm_prec")
     return out if batched else C[0]
 
 

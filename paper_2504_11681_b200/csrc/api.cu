@@ -451,6 +451,21 @@ int tfno_fft_execute(int n, int direction, int keep, int src_len, int64_t P, con
   return cuda_status(launch_pencils_auto(a, direction < 0 ? -1 : 1, (cudaStream_t)stream));
 }
 
+int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,
+                    int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
+                    int64_t c_ns, int64_t c_bs, float alpha, int prec, void* stream) {
+  if (prec == TFNO_FP32)
+    return tfno_cgemm(M, N, K, batch, A, a_ms, a_ks, a_bs, W, w_ks, w_ns, w_bs, C, c_ms, c_ns, c_bs, alpha, stream);
+  if (prec != TFNO_TF32 && prec != TFNO_TF32X3) return TFNO_EUNSUPPORTED;
+  if (M < 0 || N < 0 || K < 0 || batch < 0) return TFNO_EINVAL;
+  if (M == 0 || N == 0 || batch == 0) return TFNO_OK;
+  if (!A || !W || !C) return TFNO_EINVAL;
+  GemmArgs g{M, N, K, batch, (const float2*)A, a_ms, a_ks, a_bs, (const float2*)W, w_ks, w_ns, w_bs,
+             (float2*)C, c_ms, c_ns, c_bs, alpha};
+  if (!cgemm_tc_supported(g)) return TFNO_EUNSUPPORTED;
+  return cuda_status(launch_cgemm_prec(g, prec, (cudaStream_t)stream));
+}
+
 int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,
                int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
                int64_t c_ns, int64_t c_bs, float alpha, void* stream) {
@@ -527,7 +542,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
                        void* wsv, size_t ws_bytes, void* stream) {
   if (!c || mode < TFNO_STAGED || mode > TFNO_FULLY_FUSED) return TFNO_EINVAL;
   if (tfno_config_violations(c, nullptr, 8)) return TFNO_EINVAL;
-  if (prec != TFNO_FP32 && !(prec == TFNO_TF32 || prec == TFNO_BF16)) return TFNO_EINVAL;
+  if (prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3) return prec == TFNO_BF16 ? TFNO_EUNSUPPORTED : TFNO_EINVAL;
   if (!xv || !wv || !yv) return TFNO_EINVAL;
   if (c->dim_x > TFNO_TW_MAX || c->dim_y > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
@@ -621,7 +636,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     GemmArgs ga{g.kx * g.ky, g.N, g.H, g.B, A, 1, g.kx * g.ky, g.H * g.kx * g.ky, w, g.N, 1, 0,
                 Cm, 1, g.kx * g.ky, g.N * g.kx * g.ky, 1.0f};
     if (g.B > 65535) return TFNO_EUNSUPPORTED;
-    if ((e = launch_cgemm(ga, st)) != cudaSuccess) return TFNO_ECUDA;
+    if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e == cudaErrorNotSupported ? TFNO_EUNSUPPORTED : TFNO_ECUDA;
     stage_mark(st);
   }
   if (!s.gi) {

@@ -1,0 +1,326 @@
+// tcgen05 (5th-gen tensor core) mode contraction for sm_100a:
+//   C[b][n][m] = alpha * sum_h A[b][h][m] * W[h][n]      (complex64)
+// the channel mix of the Fourier layer (pipeline.py:198-199, cgemm.py:83-95)
+// for the TF32 / 3xTF32 precisions (BASELINE C5: "TF32/BF16 tcgen05 CGEMM
+// variant vs FP32").
+//
+// Real embedding without re-layout: K' = 2h + c (c = re/im of A), N' = 2n + c',
+//   W'[2h+c][2n+c'] = [[Wr, Wi], [-Wi, Wr]][c][c'],
+// so D[m][2n+c'] = (Re, Im) of C[m][n] and an interleaved complex64 A row
+// pair is exactly two K' rows.  Per CTA: M tile of 128 modes (TMEM lanes),
+// D = 128 x N' fp32 in TMEM (N' = 2N <= 256 columns), K' streamed in chunks
+// of 32 through a 2-stage shared-memory ring in the K-major SWIZZLE_NONE
+// canonical layout (core matrix = 8 MN rows x 4 K fp32 = 128 B; SBO = 128 B
+// between MN groups, LBO between K groups).  One elected thread issues
+// tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=N', K=8) x 4 per chunk
+// (x3 for 3xTF32: hi*hi + hi*lo + lo*hi, lo = x - tf32(x)) and
+// tcgen05.commit's to the stage's mbarrier; the next chunk's global loads are
+// already in flight in registers.  Epilogue: tcgen05.ld 32x32b.x32 -> alpha
+// -> coalesced complex stores.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tfno {
+
+namespace tc {
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (Blackwell)
+  // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K- or MN-major, M, N
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool kmajor) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((kmajor ? 0u : 1u) << 15) | ((kmajor ? 0u : 1u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TCW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TCW_%=;\n}" ::"r"(saddr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// tf32 split: hi keeps the 10 explicit mantissa bits, lo = x - hi (exact in fp32)
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+}  // namespace tc
+
+constexpr int TC_BM = 128, TC_BK = 32;  // M tile (TMEM lanes), K' chunk
+
+template <int NP>
+struct TcGeo {
+  static constexpr int A_TILE = TC_BM * TC_BK * 4;  // bytes of one A tile (hi or lo)
+  static constexpr int B_TILE = NP * TC_BK * 4;
+  // K-group stride inside a tile: MN-major groups of 8 K hold E/4 core matrices,
+  // K-major groups of 4 K hold E/8 core matrices
+  static constexpr int TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+};
+
+// byte offset of element (mn, k) in a no-swizzle canonical tile:
+//   MN-major core matrix = 4 MN (16 B contiguous) x 8 K rows; MN groups at
+//   128 B, K groups at `lbo`.
+//   K-major  core matrix = 8 MN rows x 4 K (16 B contiguous); MN groups at
+//   128 B, K groups (of 4) at `lbo`.
+// byte offset of element (mn, k) in the K-major SWIZZLE_NONE canonical tile:
+// core matrix = 8 MN rows x 4 K (16 B contiguous per row, 128 B per core
+// matrix); MN groups at SBO = 128 B, K groups (of 4) at LBO = (E/8)*128 B.
+// (The MN-major no-swizzle variant was probed and rejected on B200 for tf32.)
+__device__ __forceinline__ uint32_t cm_off(int mn, int k, int lbo) {
+  return (uint32_t)((k >> 2) * lbo + (mn >> 3) * 128 + (mn & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ float4 hi4(float4 v) {
+  return make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
+}
+__device__ __forceinline__ float4 sub4(float4 a, float4 b) {
+  return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+}
+
+template <int NP, int PASSES>
+__global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
+  using Gm = TcGeo<NP>;
+  constexpr int A_LBO = (TC_BM / 8) * 128, B_LBO = (NP / 8) * 128;
+  constexpr int STAGE = (PASSES > 1 ? 2 : 1) * (Gm::A_TILE + Gm::B_TILE);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;  // 2 stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = g.M, N = g.N, K = g.K;  // complex dims: modes, out channels, hidden
+  const int mtiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int64_t tiles = (int64_t)mtiles * g.batch;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);  // K' = 2K real, 16 channels per chunk
+
+  if (tid == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::saddr(tmem_slot)),
+                 "n"(Gm::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t IDESC = tc::make_idesc(TC_BM, NP, true);
+
+  // chunk = 16 channels = 8 channel pairs.  A item (m, pair): A[h][m], A[h+1][m]
+  // -> one K-major row (re_h, im_h, re_h+1, im_h+1).  B item (n, pair):
+  // W[h][n], W[h+1][n] -> rows n' = 2n (Wr, -Wi, ...) and 2n+1 (Wi, Wr, ...).
+  constexpr int AI = TC_BM * 8 / 128;       // 8 A items per thread
+  constexpr int BI = (NP / 2) * 8 / 128;    // B items per thread (NP/32)
+  float4 ra[AI], rb[BI];
+
+  auto load_chunk = [&](int64_t tile, int c) {
+    const int64_t b = tile / mtiles;
+    const int64_t m0 = (tile % mtiles) * TC_BM;
+    const int64_t h0 = (int64_t)c * (TC_BK / 2);
+    const float2* Ab = g.A + b * g.a_bs;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 128;
+      const int ml = idx % TC_BM, hp = idx / TC_BM;
+      const int64_t m = m0 + ml, h = h0 + 2 * hp;
+      const float2 v0 = (m < M && h < K) ? __ldg(Ab + h * g.a_ks + m) : make_float2(0.f, 0.f);
+      const float2 v1 = (m < M && h + 1 < K) ? __ldg(Ab + (h + 1) * g.a_ks + m) : make_float2(0.f, 0.f);
+      ra[i] = make_float4(v0.x, v0.y, v1.x, v1.y);
+    }
+#pragma unroll
+    for (int i = 0; i < BI; ++i) {
+      const int idx = tid + i * 128;
+      const int nl = idx % (NP / 2), hp = idx / (NP / 2);
+      const int64_t h = h0 + 2 * hp;
+      const float2 w0 = (nl < N && h < K) ? __ldg(g.W + h * g.w_ks + nl) : make_float2(0.f, 0.f);
+      const float2 w1 = (nl < N && h + 1 < K) ? __ldg(g.W + (h + 1) * g.w_ks + nl) : make_float2(0.f, 0.f);
+      rb[i] = make_float4(w0.x, w0.y, w1.x, w1.y);
+    }
+  };
+  auto store_chunk = [&](int st) {
+    uint8_t* sA = stage_base + st * STAGE;
+    uint8_t* sB = sA + Gm::A_TILE;
+    uint8_t* sAl = sB + Gm::B_TILE;
+    uint8_t* sBl = sAl + Gm::A_TILE;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 128;
+      const int ml = idx % TC_BM, hp = idx / TC_BM;
+      const uint32_t o = cm_off(ml, 4 * hp, A_LBO);
+      if (PASSES == 1) {
+        *reinterpret_cast<float4*>(sA + o) = ra[i];
+      } else {
+        const float4 h = hi4(ra[i]);
+        *reinterpret_cast<float4*>(sA + o) = h;
+        *reinterpret_cast<float4*>(sAl + o) = sub4(ra[i], h);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BI; ++i) {
+      const int idx = tid + i * 128;
+      const int nl = idx % (NP / 2), hp = idx / (NP / 2);
+      const float4 w = rb[i];  // (Wr_h, Wi_h, Wr_h+1, Wi_h+1)
+      const float4 re_row = make_float4(w.x, -w.y, w.z, -w.w);  // n' = 2n   (c' = 0)
+      const float4 im_row = make_float4(w.y, w.x, w.w, w.z);    // n' = 2n+1 (c' = 1)
+      const uint32_t o0 = cm_off(2 * nl, 4 * hp, B_LBO), o1 = cm_off(2 * nl + 1, 4 * hp, B_LBO);
+      if (PASSES == 1) {
+        *reinterpret_cast<float4*>(sB + o0) = re_row;
+        *reinterpret_cast<float4*>(sB + o1) = im_row;
+      } else {
+        const float4 h0 = hi4(re_row), h1 = hi4(im_row);
+        *reinterpret_cast<float4*>(sB + o0) = h0;
+        *reinterpret_cast<float4*>(sB + o1) = h1;
+        *reinterpret_cast<float4*>(sBl + o0) = sub4(re_row, h0);
+        *reinterpret_cast<float4*>(sBl + o1) = sub4(im_row, h1);
+      }
+    }
+  };
+
+  int64_t gch = 0;  // global chunk counter (stage = gch & 1, parity = (gch >> 1) & 1)
+  int64_t tile = blockIdx.x;
+  if (tile < tiles) load_chunk(tile, 0);
+  for (; tile < tiles; tile += gridDim.x) {
+    for (int c = 0; c < nchunks; ++c, ++gch) {
+      const int st = (int)(gch & 1);
+      if (gch >= 2) tc::mbar_wait(&bars[st], (uint32_t)(((gch - 2) >> 1) & 1));  // stage free
+      store_chunk(st);
+      // next chunk (or the first chunk of the next tile) in flight during the MMAs
+      if (c + 1 < nchunks)
+        load_chunk(tile, c + 1);
+      else if (tile + gridDim.x < tiles)
+        load_chunk(tile + gridDim.x, 0);
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        const uint32_t a0 = tc::saddr(stage_base + st * STAGE);
+        const uint32_t b0 = a0 + Gm::A_TILE;
+        const uint32_t al = b0 + Gm::B_TILE, bl = al + Gm::A_TILE;
+#pragma unroll
+        for (int s = 0; s < TC_BK / 8; ++s) {  // K = 8 per MMA = 2 K groups
+          const uint64_t ad = tc::make_desc(a0 + 2 * s * A_LBO, A_LBO, 128);
+          const uint64_t bd = tc::make_desc(b0 + 2 * s * B_LBO, B_LBO, 128);
+          tc::mma_tf32(tmem, ad, bd, IDESC, (c > 0 || s > 0) ? 1u : 0u);
+          if (PASSES > 1) {
+            const uint64_t adl = tc::make_desc(al + 2 * s * A_LBO, A_LBO, 128);
+            const uint64_t bdl = tc::make_desc(bl + 2 * s * B_LBO, B_LBO, 128);
+            tc::mma_tf32(tmem, ad, bdl, IDESC, 1u);
+            tc::mma_tf32(tmem, adl, bd, IDESC, 1u);
+          }
+        }
+        tc::commit(&bars[st]);
+      }
+    }
+    // epilogue: wait for the tile's last MMA batch, TMEM -> registers -> C
+    {
+      const int64_t last = gch - 1;
+      tc::mbar_wait(&bars[last & 1], (uint32_t)((last >> 1) & 1));
+      tc::fence_after();
+      const int64_t b = tile / mtiles;
+      const int64_t m = (tile % mtiles) * TC_BM + warp * 32 + lane;
+      float2* Cb = g.C + b * g.c_bs;
+#pragma unroll 1
+      for (int col = 0; col < NP; col += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + col, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t n = col / 2 + q;
+          if (m < M && n < N) Cb[n * g.c_ns + m] = make_float2(g.alpha * v[2 * q], g.alpha * v[2 * q + 1]);
+        }
+      }
+      tc::fence_before();
+      __syncthreads();  // TMEM reads done before the next tile's first MMA overwrites D
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
+}
+
+template <int NP, int PASSES>
+static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
+  constexpr int STAGE = (PASSES > 1 ? 2 : 1) * (TcGeo<NP>::A_TILE + TcGeo<NP>::B_TILE);
+  const size_t smem = 2 * STAGE + 64;
+  cudaError_t e =
+      cudaFuncSetAttribute(cgemm_tc_kernel<NP, PASSES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * g.batch;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  cgemm_tc_kernel<NP, PASSES><<<grid, 128, smem, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+bool cgemm_tc_supported(const GemmArgs& g) {
+  return g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.N >= 1 && g.N <= 128;
+}
+
+cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s) {
+  if (!cgemm_tc_supported(g)) return cudaErrorNotSupported;
+  const int np = (int)(2 * g.N);
+  if (passes == 1) {
+    if (np <= 64) return launch_tc_t<64, 1>(g, s);
+    if (np <= 128) return launch_tc_t<128, 1>(g, s);
+    return launch_tc_t<256, 1>(g, s);
+  }
+  if (np <= 64) return launch_tc_t<64, 3>(g, s);
+  if (np <= 128) return launch_tc_t<128, 3>(g, s);
+  return launch_tc_t<256, 3>(g, s);
+}
+
+}  // namespace tfno

@@ -58,6 +58,15 @@ size_t fft_pencils_smem_bytes(int n, int PB, int pencil_major);
 
 cudaError_t launch_fft_pencils(const FftPencilArgs& a, int dir, cudaStream_t s);
 cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s);
+// tcgen05 TF32 contraction (cgemm_tc.cu): passes 1 = TF32, 3 = 3xTF32 (fp32-level accuracy)
+bool cgemm_tc_supported(const GemmArgs& g);
+cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s);
+// precision dispatch: 0 FP32 SIMT, 1 TF32 tcgen05, 3 3xTF32 tcgen05
+inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s) {
+  if (prec == 0) return launch_cgemm(g, s);
+  if (prec == 1 || prec == 3) return launch_cgemm_tc(g, prec == 1 ? 1 : 3, s);
+  return cudaErrorNotSupported;
+}
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
 cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,
                                 float2* dst, int dx2, int dy2, int64_t d_plane, int cx, int cy,

@@ -1,0 +1,45 @@
+"""GPU: the tcgen05 (tensor-core) contraction.  Stated tolerances
+(BASELINE.md §5): 3xTF32 <= 1e-5 (fp32-level), TF32 <= 1e-3 at the layer."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2504_11681_b200 as T
+    from oracle import fnofuse_port as O
+    return T, O, torch
+
+
+@pytest.mark.parametrize("M,N,K,B", [(4096, 128, 128, 2), (1024, 64, 64, 3), (256, 64, 64, 2), (300, 37, 20, 2),
+                                     (32, 64, 64, 4), (129, 1, 3, 1), (128, 128, 256, 1)])
+@pytest.mark.parametrize("prec,tol", [("tf32x3", 1e-5), ("tf32", 2e-3)])
+def test_tc_cgemm_vs_float64(env, M, N, K, B, prec, tol):
+    T, O, torch = env
+    rng = np.random.default_rng(M + N + K)
+    a = (rng.standard_normal((B, K, M)) + 1j * rng.standard_normal((B, K, M))).astype(np.complex64)
+    w = (rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))).astype(np.complex64)
+    A = torch.from_numpy(a).cuda().transpose(1, 2)            # [B, M, K] view, m contiguous
+    W = torch.from_numpy(w).cuda()
+    out = torch.empty((B, N, M), dtype=torch.complex64, device="cuda").transpose(1, 2)
+    C = T.cgemm_device(A, W, out=out, alpha=0.5, precision=prec)
+    want = 0.5 * np.einsum("bkm,kn->bmn", a.astype(np.complex128), w.astype(np.complex128))
+    assert T.max_rel_error(C.cpu().numpy(), want) < tol
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 8, 512, 512, 64, 64, 2), (3, 16, 8, 256, 256, 32, 32, 2),
+                                   (2, 8, 16, 256, 256, 16, 16, 2), (3, 12, 20, 1, 1024, 1, 128, 1)])
+def test_layer_tensorcore_precisions(env, shape):
+    T, O, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = O.random_inputs(cfg, 8)
+    ref = O.run_layer_values(cfg, x, w)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    mode = "fully_fused" if cfg.rank == 2 else "fft_optimized"
+    for prec, tol in (("tf32x3", 1e-5), ("tf32", 1e-3)):
+        y = T.run_layer_device(cfg, xd, wd, mode=mode, precision=prec)
+        assert T.max_rel_error(y.cpu().numpy(), ref) < tol, prec

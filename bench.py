@@ -41,7 +41,10 @@ WORKLOADS = {
     "C3": (32, 64, 64, 256, 256, 32, 32, 2, "C3: 2D FNO layer b32 256x256 H64->64 modes 32x32"),
     "C4": (128, 128, 128, 512, 512, 64, 64, 2, "C4: 2D FNO layer b128 512x512 H128->128 modes 64x64"),
     "C5L": (256, 64, 64, 256, 256, 16, 16, 2, "C5 single layer: 2D b256 256x256 W64 modes 16x16"),
+    "C5": (256, 64, 64, 256, 256, 16, 16, 2, "C5: 4-layer 2D FNO forward b256 256x256 W64 modes 16x16 "
+                                             "(one CUDA graph, 12 kernels)"),
 }
+LAYERS = {"C5": 4}
 for _n in (256, 1024, 4096):
     for _h in (64, 128, 256):
         for _b in (64, 256, 1024):
@@ -174,11 +177,24 @@ def run_reference_arm(args):
     B, H, N, dx, dy, kx, ky, rk, desc = WORKLOADS[args.workload]
     workers = len(os.sched_getaffinity(0))
     sb = max(1, min(B, workers))
-    scfg = T.FnoLayerConfig(sb, H, N, dx, dy, kx, ky, rk)
-    x, w = O.random_inputs(scfg, 1234)
-    flops = T.layer_flops(scfg)["flops"]
     pool = O.CpuPool(workers)
     from types import SimpleNamespace
+    # bound the whole run to ~budget_s: calibrate one batch element per worker
+    # on an 8-channel sample, then pick the channel count per step (same
+    # per-channel work as the workload; flops counted for the exact sample)
+    budget_s = float(os.environ.get("TFNO_REF_BUDGET_S", "150"))
+    ch = min(8, H, N)
+    ccal = T.FnoLayerConfig(sb, ch, ch, dx, dy, kx, ky, rk)
+    xc, wc = O.random_inputs(ccal, 1)
+    t0 = time.perf_counter()
+    pool.run(SimpleNamespace(**ccal.__dict__), xc, wc)
+    t_cal = time.perf_counter() - t0
+    per_step = budget_s / max(1, args.steps + args.warmup)
+    scale = max(1.0, per_step / max(t_cal, 1e-3))
+    hs, ns = min(H, max(ch, int(ch * scale))), min(N, max(ch, int(ch * scale)))
+    scfg = T.FnoLayerConfig(sb, hs, ns, dx, dy, kx, ky, rk)
+    x, w = O.random_inputs(scfg, 1234)
+    flops = T.layer_flops(scfg)["flops"]
     c = SimpleNamespace(**scfg.__dict__)
     for _ in range(args.warmup):
         pool.run(c, x, w)
@@ -188,13 +204,14 @@ def run_reference_arm(args):
     dt = (time.perf_counter() - t0) / args.steps
     pool.close()
     val = flops / dt / 1e9
-    sample = f"batch {sb} of {args.workload} per step (1 batch element per worker), numpy oracle port of fnofuse"
+    sample = (f"{sb} batch elements x {hs}->{ns} channels of {args.workload} per step (1 batch element per "
+              f"worker process), numpy oracle port of fnofuse (bitwise equal to the reference)")
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-            "us_per_layer_extrapolated": round(dt * 1e6 * B / sb, 1),
+            "us_per_layer_extrapolated": round(dt * 1e6 * T.layer_flops(T.FnoLayerConfig(B, H, N, dx, dy, kx, ky, rk))["flops"] / flops, 1),
             "higher_is_better": True, "scaling": "n/a (CPU)", "vs_baseline": None, "dtype": "fp32 (complex64)",
             "data": "synthetic (seeded N(0,1))",
-            "config": {"workload": desc, "batch_sample": sb, "mode": "fully_fused"},
+            "config": {"workload": desc, "batch_sample": sb, "channels_sample": [hs, ns], "mode": "fully_fused"},
             "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": workers, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -264,6 +281,15 @@ def run_ours(args):
     def step():
         T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=prec, validate=False)
 
+    nlayers = LAYERS.get(args.workload, 1)
+    chain = None
+    if nlayers > 1:
+        from paper_2504_11681_b200.chain import FnoChain
+        ws_ = [w] + [torch.view_as_complex(torch.randn((H, N, 2), generator=g, device=dev,
+                                                        dtype=torch.float32)).contiguous()
+                     for _ in range(nlayers - 1)]
+        chain = FnoChain(cfg, ws_, mode=mode, precision=prec).capture(x)
+
     # ---- stage events inside the timed region (dominant-kernel roofline) ----
     nst = len(sched.split("|")) + 1
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst)] for _ in range(args.steps)]
@@ -279,8 +305,23 @@ def run_ours(args):
         step()
         cur[0] += 1
 
+    if chain is not None:
+        # per-kernel events of one layer (graph replays carry no events), then the
+        # graph-launched chain is the timed step
+        for _ in range(args.warmup):
+            step()
+        for i in range(args.steps):
+            step_timed()
+        torch.cuda.synchronize()
+        lib.tfno_set_stage_events(None, 0)
+        layer_stage_ms = [statistics.mean(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps))
+                          for j in range(nst - 1)]
+
+        def step_timed():  # noqa: F811
+            chain.forward(x)
+
     for _ in range(args.warmup):
-        step()
+        step() if chain is None else chain.forward(x)
     torch.cuda.synchronize()
     barrier()
     clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
@@ -295,6 +336,8 @@ def run_ours(args):
     e0.record(stream)
     torch.cuda.synchronize()
     launches = lib.tfno_launch_count() - n0
+    if chain is not None:  # graph replays: the kernels were recorded once at capture
+        launches = args.steps * chain.kernels_per_forward
     lib.tfno_set_stage_events(None, 0)
     clk = clocks.stop()
     barrier()
@@ -302,9 +345,13 @@ def run_ours(args):
     ms = max_over_ranks(ms_local)
     # per-stage average durations
     names = sched.split("|")
-    stage_ms = [statistics.mean(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps))
-                for j in range(len(names))]
+    if chain is None:
+        stage_ms = [statistics.mean(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps))
+                    for j in range(len(names))]
+    else:
+        stage_ms = layer_stage_ms
     fl = T.layer_flops(cfg, mode)
+    fl = {k: v * nlayers for k, v in fl.items()} if nlayers > 1 else fl
     total_flops = fl["flops"] * ws
     value = total_flops / (ms * 1e-3) / 1e9
     hbm_peak, peak_kind, pk = peaks()
@@ -320,7 +367,7 @@ def run_ours(args):
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "us_per_layer": round(ms * 1e3, 2),
-        "layers_per_s": round(ws * 1e3 / ms, 2), "higher_is_better": True,
+        "layers_per_s": round(ws * nlayers * 1e3 / ms, 2), "higher_is_better": True,
         "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None,
         "dtype": ("fp32 (complex64 in/out, fp32 arithmetic)" if prec == "fp32" else
                   f"fp32 FFTs + {prec} tcgen05 channel contraction (complex64 in/out)"),
@@ -342,7 +389,7 @@ def run_ours(args):
                            "frac_of_roof_8TBps_74TF": round(t_roof / (ms * 1e-3), 4),
                            "frac_of_measured_hbm": round(layer_bytes / (ms * 1e-3) / 1e9 / hbm_peak, 4),
                            "achieved_GBps": round(layer_bytes / (ms * 1e-3) / 1e9, 1)},
-        "gpu_launches": int(launches), "launches_per_layer": nlaunch, "clocks": clk,
+        "gpu_launches": int(launches), "launches_per_layer": nlaunch, "layers_per_step": nlayers, "clocks": clk,
     }
 
     # ---- unfused baselines measured in the same run (rank-local, max over ranks) ----
@@ -373,8 +420,46 @@ def run_ours(args):
         del y2
         torch.cuda.empty_cache()
 
+    # ---- tensor-core contraction variants of the same layer (reported, not the headline) ----
+    if not args.no_baselines and prec == "fp32" and args.mode == "fully_fused":
+        var = {}
+        for vp in ("tf32x3", "tf32"):
+            try:
+                ms_v = max_over_ranks(time_steps(
+                    lambda vp=vp: T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=vp, validate=False),
+                    max(3, args.steps // 2), 2, stream, barrier))
+                var[vp] = {"ms": round(ms_v, 4), "GFLOPps": round(fl["flops"] * ws / (ms_v * 1e-3) / 1e9, 2),
+                           "tolerance": 1e-5 if vp == "tf32x3" else 1e-3}
+            except Exception as ex:  # noqa: BLE001
+                var[vp] = {"error": str(ex)[:200]}
+        T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=prec, validate=False)  # restore FP32 output
+        result["precision_variants"] = var
+
     # ---- end to end through the public host-buffer API ----
-    if not args.no_e2e:
+    if not args.no_e2e and chain is not None:
+        try:
+            xh = torch.empty(x.shape, dtype=torch.complex64, pin_memory=True)
+            xh.copy_(x)
+            yh = torch.empty(y.shape, dtype=torch.complex64, pin_memory=True)
+            xs_dev = torch.empty_like(x)
+            for _ in range(1):
+                xs_dev.copy_(xh, non_blocking=True)
+                yh.copy_(chain.forward(xs_dev), non_blocking=True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(max(1, args.e2e_steps)):
+                xs_dev.copy_(xh, non_blocking=True)
+                yh.copy_(chain.forward(xs_dev), non_blocking=True)
+            torch.cuda.synchronize()
+            ms_e = max_over_ranks((time.perf_counter() - t0) * 1e3 / max(1, args.e2e_steps))
+            result["e2e"] = {"value": round(fl["flops"] * ws / (ms_e * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+                             "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8),
+                             "steps": max(1, args.e2e_steps), "ms_per_step": round(ms_e, 2),
+                             "api": "pinned H2D -> FnoChain.forward (CUDA graph) -> pinned D2H"}
+            del xh, yh, xs_dev
+        except Exception as ex:  # noqa: BLE001
+            result["e2e"] = {"error": str(ex)[:300]}
+    elif not args.no_e2e:
         try:
             e2e = run_e2e(T, cfg, x, w, mode, prec, args, barrier, max_over_ranks, stream)
             e2e["value"] = round(fl["flops"] * ws / (e2e.pop("ms") * 1e-3) / 1e9, 2)
@@ -387,11 +472,18 @@ def run_ours(args):
         workers = len(os.sched_getaffinity(0))
         sb = max(1, min(B, workers))
         xs = x[:sb].cpu().numpy()
-        wh = w.cpu().numpy()
-        ys = y[:sb].cpu().numpy()
         cfg_t = dict(batch=sb, hidden_dim=H, output_dim=N, dim_x=dx, dim_y=dy, keep_x=kx, keep_y=ky, rank=rk)
-        dt, ref = cpu_reference(cfg_t, xs, wh, workers)
-        sflops = T.layer_flops(T.FnoLayerConfig(**cfg_t))["flops"]
+        if chain is None:
+            wh = w.cpu().numpy()
+            ys = y[:sb].cpu().numpy()
+            dt, ref = cpu_reference(cfg_t, xs, wh, workers)
+        else:
+            ys = chain.forward(x)[:sb].cpu().numpy()
+            dt, ref = 0.0, xs
+            for wl in chain.weights:
+                d_, ref = cpu_reference(cfg_t, ref, wl.cpu().numpy(), workers)
+                dt += d_
+        sflops = T.layer_flops(T.FnoLayerConfig(**cfg_t))["flops"] * nlayers
         result["cpu_baseline"] = {"value": round(sflops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": workers,
                                   "kind": "port",
                                   "sample": f"first {sb} batch elements of the timed input, 1 per worker process "

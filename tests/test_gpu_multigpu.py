@@ -72,3 +72,24 @@ def test_spectrum_entry_points_vs_oracle(env, shape):
     spec[:, :, :cfg.keep_x, :cfg.keep_y] = want
     yr = 2.0 * np.fft.ifft2(spec, axes=(2, 3))
     assert T.max_rel_error(y.cpu().numpy(), yr) < 1e-5
+
+
+def test_chain_graph_matches_chained_layers(env):
+    """4-layer chain (BASELINE configs[4] shape, reduced batch) captured in a
+    CUDA graph == chained reference run_layer calls (oracle)."""
+    T, O, MG, torch = env
+    from paper_2504_11681_b200.chain import FnoChain
+    cfg = T.FnoLayerConfig(2, 8, 8, 256, 256, 16, 16, rank=2)
+    x, _ = O.random_inputs(cfg, 21)
+    rng = np.random.default_rng(3)
+    ws = [(rng.standard_normal((8, 8)) + 1j * rng.standard_normal((8, 8))).astype(np.complex64) for _ in range(4)]
+    xd = torch.from_numpy(x).cuda()
+    ch = FnoChain(cfg, [torch.from_numpy(w).cuda() for w in ws]).capture(xd)
+    assert ch.kernels_per_forward == 12
+    y = ch.forward(xd).cpu().numpy()
+    ref = x
+    for w in ws:
+        ref = O.run_layer_values(cfg, ref, w)
+    assert T.max_rel_error(y, ref) < 1e-5
+    y2 = ch.forward(xd).cpu().numpy()
+    assert np.array_equal(y, y2)

@@ -130,7 +130,8 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
                int64_t c_ns, int64_t c_bs, float alpha, void* stream);
 
 /* tfno_cgemm with a contraction precision (TFNO_FP32 / TFNO_TF32 / TFNO_TF32X3).
- * The tensor-core path needs the mode layout: a_ms = c_ms = w_ns = 1, w_bs = 0, N <= 128. */
+ * The tensor-core path needs the mode layout: a_ms = c_ms = w_ns = 1, w_bs = 0 (N > 128 runs in
+ * 128-channel blocks). */
 int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,
                     int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
                     int64_t c_ns, int64_t c_bs, float alpha, int prec, void* stream);

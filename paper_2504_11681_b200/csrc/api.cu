@@ -176,9 +176,9 @@ Sched make_sched(const tfno_cfg* c, int mode) {
   int NT = 0;
   bool ok;
   if (rows_tiling((int)g.dy, (int)g.ky, (int)g.N, NT)) {
-    // fused only while the C tile covers >= half of N (else the FFT would be
+    // fused only while the C tile covers all of N (else the FFT would be
     // recomputed per n-tile): otherwise the unfused schedule of fast kernels
-    ok = (g.N + NT - 1) / NT <= 2;
+    ok = (g.N + NT - 1) / NT <= 1;  // measured: a second n-tile (recomputed FFTs) loses to the unfused schedule
     s.rows_fast = ok;
     s.rows_NT = NT;
   } else {

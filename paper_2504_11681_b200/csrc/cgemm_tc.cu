@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = g.M, N = g.N, K = g.K;  // complex dims: modes, out channels, hidden
   const int mtiles = (int)((M + TC_BM - 1) / TC_BM);
-  const int64_t tiles = (int64_t)mtiles * g.batch;
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));    // output-channel blocks of NP/2
+  const int64_t tiles = (int64_t)mtiles * nsplit * g.batch;
   const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);  // K' = 2K real, 16 channels per chunk
 
   if (tid == 0) {
@@ -162,8 +163,9 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
   float4 ra[AI], rb[BI];
 
   auto load_chunk = [&](int64_t tile, int c) {
-    const int64_t b = tile / mtiles;
+    const int64_t b = tile / ((int64_t)mtiles * nsplit);
     const int64_t m0 = (tile % mtiles) * TC_BM;
+    const int64_t n0 = ((tile / mtiles) % nsplit) * (NP / 2);
     const int64_t h0 = (int64_t)c * (TC_BK / 2);
     const float2* Ab = g.A + b * g.a_bs;
 #pragma unroll
@@ -179,9 +181,9 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
     for (int i = 0; i < BI; ++i) {
       const int idx = tid + i * 128;
       const int nl = idx % (NP / 2), hp = idx / (NP / 2);
-      const int64_t h = h0 + 2 * hp;
-      const float2 w0 = (nl < N && h < K) ? __ldg(g.W + h * g.w_ks + nl) : make_float2(0.f, 0.f);
-      const float2 w1 = (nl < N && h + 1 < K) ? __ldg(g.W + (h + 1) * g.w_ks + nl) : make_float2(0.f, 0.f);
+      const int64_t h = h0 + 2 * hp, n = n0 + nl;
+      const float2 w0 = (n < N && h < K) ? __ldg(g.W + h * g.w_ks + n) : make_float2(0.f, 0.f);
+      const float2 w1 = (n < N && h + 1 < K) ? __ldg(g.W + (h + 1) * g.w_ks + n) : make_float2(0.f, 0.f);
       rb[i] = make_float4(w0.x, w0.y, w1.x, w1.y);
     }
   };
@@ -264,7 +266,8 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
       const int64_t last = gch - 1;
       tc::mbar_wait(&bars[last & 1], (uint32_t)((last >> 1) & 1));
       tc::fence_after();
-      const int64_t b = tile / mtiles;
+      const int64_t b = tile / ((int64_t)mtiles * nsplit);
+      const int64_t n0 = ((tile / mtiles) % nsplit) * (NP / 2);
       const int64_t m = (tile % mtiles) * TC_BM + warp * 32 + lane;
       float2* Cb = g.C + b * g.c_bs;
 #pragma unroll 1
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
         tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + col, v);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const int64_t n = col / 2 + q;
+          const int64_t n = n0 + col / 2 + q;
           if (m < M && n < N) Cb[n * g.c_ns + m] = make_float2(g.alpha * v[2 * q], g.alpha * v[2 * q + 1]);
         }
       }
@@ -299,7 +302,7 @@ static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * g.batch;
+  const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * ((g.N + NP / 2 - 1) / (NP / 2)) * g.batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
   cgemm_tc_kernel<NP, PASSES><<<grid, 128, smem, s>>>(g);
   ++g_launches;
@@ -307,7 +310,7 @@ static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
 }
 
 bool cgemm_tc_supported(const GemmArgs& g) {
-  return g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.N >= 1 && g.N <= 128;
+  return g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.N >= 1;
 }
 
 cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s) {

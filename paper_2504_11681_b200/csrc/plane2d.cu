@@ -258,9 +258,14 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
     team_sync<M>(team);
     // ---- sum over a: X[r + 8t] for the thread's storage column q' = tt
     if (tt < KY) {
-      float2 sacc = redt[rq * RS + tq];
+      float2 part[A];
 #pragma unroll
-      for (int a = 1; a < A; ++a) sacc = cadd(sacc, redt[rq * RS + a * RT + tq]);
+      for (int a = 0; a < A; ++a) part[a] = redt[rq * RS + a * RT + tq];
+#pragma unroll
+      for (int w = 1; w < A; w *= 2)  // tree: log2(A) dependent adds instead of A-1
+#pragma unroll
+        for (int a = 0; a < A; a += 2 * w) part[a] = cadd(part[a], part[a + w]);
+      const float2 sacc = part[0];
       const int x1 = j * TEAMS + team;
       Tc[x1 * KY + tt] = sacc;
     }

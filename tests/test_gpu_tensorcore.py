@@ -15,7 +15,7 @@ def env():
     return T, O, torch
 
 
-@pytest.mark.parametrize("M,N,K,B", [(4096, 128, 128, 2), (1024, 64, 64, 3), (256, 64, 64, 2), (300, 37, 20, 2),
+@pytest.mark.parametrize("M,N,K,B", [(4096, 128, 128, 2), (512, 256, 256, 2), (200, 300, 40, 1), (1024, 64, 64, 3), (256, 64, 64, 2), (300, 37, 20, 2),
                                      (32, 64, 64, 4), (129, 1, 3, 1), (128, 128, 256, 1)])
 @pytest.mark.parametrize("prec,tol", [("tf32x3", 1e-5), ("tf32", 2e-3)])
 def test_tc_cgemm_vs_float64(env, M, N, K, B, prec, tol):
@@ -32,7 +32,7 @@ def test_tc_cgemm_vs_float64(env, M, N, K, B, prec, tol):
 
 
 @pytest.mark.parametrize("shape", [(2, 8, 8, 512, 512, 64, 64, 2), (3, 16, 8, 256, 256, 32, 32, 2),
-                                   (2, 8, 16, 256, 256, 16, 16, 2), (3, 12, 20, 1, 1024, 1, 128, 1)])
+                                   (2, 8, 16, 256, 256, 16, 16, 2), (3, 12, 20, 1, 1024, 1, 128, 1), (2, 256, 256, 1, 256, 1, 32, 1)])
 def test_layer_tensorcore_precisions(env, shape):
     T, O, torch = env
     cfg = T.FnoLayerConfig(*shape)

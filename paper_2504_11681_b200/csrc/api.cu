@@ -139,6 +139,9 @@ bool rows_tiling(int n, int keep, int N, int& NT) {
 // compile-time row kernel, everything else to the general pencil kernel
 cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st) {
   const bool rows = a.im.P0 == 1 && a.im.s0 == 0 && a.im.es == 1 && a.om.P0 == 1 && a.om.s0 == 0 && a.om.es == 1;
+  const int dir_ = dir < 0 ? -1 : 1;
+  if (rows && warp_fft_supported(a.n, dir_, a.keep, a.src_len))
+    return launch_warp_fft(a.n, dir_, a.in, a.im.s1, a.out, a.om.s1, a.P, a.keep, a.src_len, a.scale, a.twg, st);
   if (rows && rows_supported(a.n))
     return launch_rows_fft(a.n, dir, a.in, a.im.s1, a.out, a.om.s1, a.P, a.keep, a.src_len, a.scale, a.twg, st);
   return launch_fft_pencils(a, dir, st);
@@ -146,7 +149,7 @@ cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st
 
 // schedule decision shared by workspace sizing and the forward
 struct Sched {
-  bool staged = false, plane2d = false, rows_fast = false;
+  bool staged = false, plane2d = false, rows_fast = false, warp_fused = false;
   int rows_NT = 0;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
@@ -175,6 +178,14 @@ Sched make_sched(const tfno_cfg* c, int mode) {
   FusedArgs fa{};
   int NT = 0;
   bool ok;
+  if (mode == TFNO_FULLY_FUSED && warp_fused_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
+    s.warp_fused = true;
+    s.fg = s.gi = true;
+    s.need_s1 = s.need_mid = (g.rank == 2);
+    s.launches = (g.rank == 2) ? 3 : 1;
+    s.desc = g.rank == 2 ? "x-fft|fused-fft-cgemm-ifft|x-ifft" : "fused-fft-cgemm-ifft";
+    return s;
+  }
   if (rows_tiling((int)g.dy, (int)g.ky, (int)g.N, NT)) {
     // fused only while the C tile covers all of N (else the FFT would be
     // recomputed per n-tile): otherwise the unfused schedule of fast kernels
@@ -595,11 +606,11 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   }
   if (s.fg || s.gi) {
     FusedArgs fa{};
-    if (s.rows_fast) {
+    if (s.rows_fast || s.warp_fused) {
       fa.n = (int)g.dy;
       fa.keep = (int)g.ky;
       fa.N = (int)g.N;
-      fa.NT = s.rows_NT;
+      fa.NT = s.warp_fused ? (int)g.N : s.rows_NT;
       fa.KC = rows_chunk((int)g.dy);
       fa.EC = fa.KC;
     } else {
@@ -628,7 +639,8 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     fa.twg = tw;
     fa.inv_scale = (float)(1.0 / (double)g.dy);
     if (fa.G > 2147483647LL || (g.N + fa.NT - 1) / fa.NT > 65535) return TFNO_EUNSUPPORTED;
-    e = s.rows_fast ? launch_rows_fused(fa, s.fg, s.gi, st) : launch_fused(fa, s.fg, s.gi, st);
+    e = s.warp_fused ? launch_warp_fused(fa, st)
+                     : (s.rows_fast ? launch_rows_fused(fa, s.fg, s.gi, st) : launch_fused(fa, s.fg, s.gi, st));
     if (e != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   } else {

@@ -68,6 +68,13 @@ inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s
   return cudaErrorNotSupported;
 }
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
+// warp-synchronous register FFT rows (warpfft.cu): n in {256, 1024}, keep / src_len <= n/4
+bool warp_fft_supported(int n, int dir, int keep, int src_len);
+cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2* out, int64_t os, int64_t P,
+                            int keep, int src_len, float scale, const float2* tw, cudaStream_t s);
+// fully fused 1D layer on warp FFTs (K6): whole k-loop per CTA, W resident in smem
+bool warp_fused_supported(int n, int keep, int H, int NO);
+cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,
                                 float2* dst, int dx2, int dy2, int64_t d_plane, int cx, int cy,
                                 float scale, cudaStream_t s);

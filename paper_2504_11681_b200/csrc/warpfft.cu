@@ -1,0 +1,450 @@
+// Warp-synchronous register FFTs for contiguous rows of length N = L*L
+// (L = 16: N = 256, half-warp per row; L = 32: N = 1024, one warp per row).
+//
+// Row index n = t + L*j (lane t holds its L values j in registers, loaded
+// coalesced straight from HBM).  Forward, first `keep` bins (fft.py
+// truncation semantics):
+//   stage 1  Y_t[k1] = DFT_L over j of x[t + L j]   (in registers)
+//            Y_t[k1] *= w_N^{t k1}                    (per-lane twiddles from a
+//                                                      [k1][t] smem table: no conflicts)
+//   transpose through a padded per-row smem tile (the only smem round trip)
+//   stage 2  X[k1 + L k2] = DFT_L over t of Y_t[k1], lane k1 keeps k2 < ceil(keep/L)
+// Inverse (zero-padded from src_len, x 1/N) mirrors it: lane k1 gathers its
+// nonzero inputs X[k1 + L k2], padded DFT_L over k2 -> t, twiddle w_N^{+k1 t},
+// transpose, DFT_L over k1 -> j, store y[t + L j].
+// No CTA barriers: every row lives in one (half-)warp (__syncwarp only).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tfno {
+namespace wf {
+
+// natural-order in-register DFT of length L (16 or 32): L = P*8,
+// x[n1 + P n2] -> DFT8 over n2 -> twiddle w_L^{n1 k2} -> DFT_P over n1,
+// output k = k2 + 8 k1.  v is overwritten with the natural-order output.
+template <int L, int DIR>
+__device__ __forceinline__ void dftL(float2* v, const float2* __restrict__ twL /* w_L^k, k < L (forward sign) */) {
+  constexpr int P = L / 8;
+  float2 a[P][8];
+#pragma unroll
+  for (int n1 = 0; n1 < P; ++n1) {
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) a[n1][n2] = v[n1 + P * n2];
+    dft8<DIR>(a[n1]);
+  }
+#pragma unroll
+  for (int n1 = 1; n1 < P; ++n1)
+#pragma unroll
+    for (int k2 = 1; k2 < 8; ++k2) a[n1][k2] = cmul(a[n1][k2], tw_dir<DIR>(twL[n1 * k2]));
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    float2 b[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) b[n1] = a[n1][k2];
+    dft<P, DIR>(b);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) v[k2 + 8 * k1] = b[k1];
+  }
+}
+
+// first KP outputs of a forward DFT_L (KP <= 8): sum over n1 of the twiddled
+// DFT8 outputs (k1 = 0 of the second factor)
+template <int L, int KP>
+__device__ __forceinline__ void dftL_first(const float2* v, float2* out, const float2* __restrict__ twL) {
+  constexpr int P = L / 8;
+  float2 a[P][8];
+#pragma unroll
+  for (int n1 = 0; n1 < P; ++n1) {
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) a[n1][n2] = v[n1 + P * n2];
+    dft8<-1>(a[n1]);
+  }
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    float2 s = a[0][k];
+#pragma unroll
+    for (int n1 = 1; n1 < P; ++n1) s = cadd(s, k ? cmul(a[n1][k], twL[n1 * k]) : a[n1][k]);
+    out[k] = s;
+  }
+}
+
+// inverse DFT_L with only the first KP inputs nonzero (KP <= 8):
+// z[t_lo + 8 t_hi] = sum_k (x[k] w_L^{+k t_lo}) w_P^{+k t_hi}, P = L/8: per t_lo
+// twiddle the KP inputs, fold k -> k mod P, inverse DFT_P over k mod P -> t_hi.
+template <int L, int KP>
+__device__ __forceinline__ void idftL_padded(const float2* x, float2* out, const float2* __restrict__ twL) {
+  constexpr int P = L / 8;
+  static_assert(KP <= 8, "padded inputs");
+#pragma unroll
+  for (int tl = 0; tl < 8; ++tl) {
+    float2 f[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) f[r] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int e = (k * tl) % L;
+      const float2 xk = e ? cmul(x[k], conjf2(twL[e])) : x[k];
+      f[k % P] = cadd(f[k % P], xk);
+    }
+    dft<P, 1>(f);
+#pragma unroll
+    for (int th = 0; th < P; ++th) out[tl + 8 * th] = f[th];
+  }
+}
+
+}  // namespace wf
+
+template <int L>
+struct WfGeo {
+  static constexpr int N = L * L;
+  static constexpr int NTH = 256;
+  static constexpr int ROWS = NTH / L;        // rows in flight per CTA pass
+  static constexpr int TSTR = L + 1;          // padded transpose stride (complex)
+  static constexpr size_t smem_bytes() {
+    return sizeof(float2) * ((size_t)L + (size_t)L * L + (size_t)ROWS * L * TSTR);
+  }
+};
+
+// forward: rows [P][src stride] -> out [P][keep] (out stride), src_len = N
+template <int L, int KP>
+__global__ void __launch_bounds__(WfGeo<L>::NTH) warp_fft_fwd_kernel(const float2* __restrict__ in,
+                                                                   int64_t in_stride, float2* __restrict__ out,
+                                                                   int64_t out_stride, int64_t P, int keep,
+                                                                   const float2* __restrict__ twg) {
+  using G = WfGeo<L>;
+  constexpr int N = G::N;
+  extern __shared__ __align__(16) float2 sm[];
+  float2* twL = sm;                 // w_L^k
+  float2* twN = twL + L;            // [k1][t] = w_N^{t k1}
+  float2* tr = twN + L * L;         // ROWS x L x TSTR
+  const int tid = threadIdx.x, lane = tid % L, rloc = tid / L;
+  const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (rloc & 1)));
+  for (int k = tid; k < L; k += G::NTH) twL[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / L)]);
+  for (int i = tid; i < L * L; i += G::NTH) {
+    const int k1 = i / L, t = i % L;
+    twN[i] = __ldg(&twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
+  }
+  __syncthreads();
+  float2* trr = tr + rloc * L * G::TSTR;
+  for (int64_t row = (int64_t)blockIdx.x * G::ROWS + rloc; row < P; row += (int64_t)gridDim.x * G::ROWS) {
+    const float2* src = in + row * in_stride;
+    float2 v[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) v[j] = __ldg(&src[lane + L * j]);
+    wf::dftL<L, -1>(v, twL);
+#pragma unroll
+    for (int k1 = 1; k1 < L; ++k1) v[k1] = cmul(v[k1], twN[k1 * L + lane]);  // consecutive lanes
+    __syncwarp(tmask);
+#pragma unroll
+    for (int k1 = 0; k1 < L; ++k1) trr[k1 * G::TSTR + lane] = v[k1];
+    __syncwarp(tmask);
+    // lane = k1 now: gather Y_t[k1] over t, first KP outputs of DFT_L over t
+#pragma unroll
+    for (int t = 0; t < L; ++t) v[t] = trr[lane * G::TSTR + t];
+    float2 o[KP];
+    wf::dftL_first<L, KP>(v, o, twL);
+    float2* dst = out + row * out_stride;
+#pragma unroll
+    for (int k2 = 0; k2 < KP; ++k2) {
+      const int k = lane + L * k2;
+      if (k < keep) dst[k] = o[k2];
+    }
+  }
+}
+
+// inverse: modes [P][src_len] (src stride) -> rows [P][N] (out stride), x scale
+template <int L, int KP>
+__global__ void __launch_bounds__(WfGeo<L>::NTH) warp_fft_inv_kernel(const float2* __restrict__ in,
+                                                                   int64_t in_stride, float2* __restrict__ out,
+                                                                   int64_t out_stride, int64_t P, int src_len,
+                                                                   float scale, const float2* __restrict__ twg) {
+  using G = WfGeo<L>;
+  constexpr int N = G::N;
+  extern __shared__ __align__(16) float2 sm[];
+  float2* twL = sm;
+  float2* twN = twL + L;
+  float2* tr = twN + L * L;
+  const int tid = threadIdx.x, lane = tid % L, rloc = tid / L;
+  const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (rloc & 1)));
+  for (int k = tid; k < L; k += G::NTH) twL[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / L)]);
+  for (int i = tid; i < L * L; i += G::NTH) {
+    const int k1 = i / L, t = i % L;
+    twN[i] = __ldg(&twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
+  }
+  __syncthreads();
+  float2* trr = tr + rloc * L * G::TSTR;
+  for (int64_t row = (int64_t)blockIdx.x * G::ROWS + rloc; row < P; row += (int64_t)gridDim.x * G::ROWS) {
+    const float2* src = in + row * in_stride;
+    // lane = k1: nonzero inputs X[k1 + L k2], k2 < KP
+    float2 xk[KP];
+#pragma unroll
+    for (int k2 = 0; k2 < KP; ++k2) {
+      const int k = lane + L * k2;
+      xk[k2] = k < src_len ? __ldg(&src[k]) : make_float2(0.f, 0.f);
+    }
+    float2 z[L];
+    wf::idftL_padded<L, KP>(xk, z, twL);   // z[t] = sum_k2 X[k1 + L k2] w_L^{+k2 t}
+    // twiddle w_N^{+k1 t}; the table is symmetric (w^{t k1}), read [t][k1 = lane]: conflict-free
+#pragma unroll
+    for (int t = 1; t < L; ++t) z[t] = cmul(z[t], conjf2(twN[t * L + lane]));
+    __syncwarp(tmask);
+#pragma unroll
+    for (int t = 0; t < L; ++t) trr[t * G::TSTR + lane] = z[t];
+    __syncwarp(tmask);
+    // lane = t: DFT_L over k1 -> j, y[t + L j]
+#pragma unroll
+    for (int k1 = 0; k1 < L; ++k1) z[k1] = trr[lane * G::TSTR + k1];
+    wf::dftL<L, 1>(z, twL);
+    float2* dst = out + row * out_stride;
+#pragma unroll
+    for (int j = 0; j < L; ++j) dst[lane + L * j] = cscale(z[j], scale);
+  }
+}
+
+template <int L, int KP>
+static cudaError_t launch_wf_fwd(const float2* in, int64_t is, float2* out, int64_t os, int64_t P, int keep,
+                                 const float2* tw, cudaStream_t s) {
+  using G = WfGeo<L>;
+  const size_t smem = G::smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(warp_fft_fwd_kernel<L, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (P + G::ROWS - 1) / G::ROWS;
+  const int grid = (int)(blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8);
+  warp_fft_fwd_kernel<L, KP><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <int L, int KP>
+static cudaError_t launch_wf_inv(const float2* in, int64_t is, float2* out, int64_t os, int64_t P, int src_len,
+                                 float scale, const float2* tw, cudaStream_t s) {
+  using G = WfGeo<L>;
+  const size_t smem = G::smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(warp_fft_inv_kernel<L, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (P + G::ROWS - 1) / G::ROWS;
+  const int grid = (int)(blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8);
+  warp_fft_inv_kernel<L, KP><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, src_len, scale, tw);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- fused 1D layer
+// rows_fused on warp FFTs (K6 for N = L^2): per work item (row group g) the
+// TEAMS row-teams FFT the H channel rows straight into the smem A panel
+// As[h][q], a 256-thread register-tiled CGEMM forms C[q][n] against the
+// CTA-resident W, C goes to smem (aliasing As) and the teams run the padded
+// iFFT of every output channel row from smem to HBM.  Only x, W and y touch
+// HBM (pipeline.py:185-206, 245-250 with the whole k-loop in one CTA).
+template <int L>
+struct WfFusedGeo {
+  using G = WfGeo<L>;
+  static constexpr int NTH = 256, TEAMS = NTH / L;
+  static constexpr int TI = 4, TJ = 8;  // GEMM thread tile (q, n)
+};
+
+size_t warp_fused_smem_bytes(int n, int keep, int H, int NO) {
+  const int L = n == 256 ? 16 : 32;
+  const size_t panel = (size_t)keep * (H > NO ? H : NO);
+  return sizeof(float2) * ((size_t)L + (size_t)L * L + (size_t)(256 / L) * L * (L + 1) + panel + (size_t)H * NO);
+}
+
+template <int L, int KP>
+__global__ void __launch_bounds__(256, 1) warp_fused_kernel(FusedArgs a) {
+  using G = WfGeo<L>;
+  using F = WfFusedGeo<L>;
+  constexpr int N = G::N, TEAMS = F::TEAMS, TI = F::TI, TJ = F::TJ;
+  extern __shared__ __align__(16) float2 sm[];
+  const int keep = a.keep, H = a.H, NO = a.N;
+  float2* twL = sm;
+  float2* twN = twL + L;
+  float2* tr = twN + L * L;
+  float2* P = tr + TEAMS * L * G::TSTR;                 // As[h][q] / Cs[n][q] (aliased)
+  float2* Ws = P + (size_t)keep * (H > NO ? H : NO);    // W[h][n], CTA resident
+  const int tid = threadIdx.x, lane = tid % L, team = tid / L;
+  const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));  // this team's lanes
+  for (int k = tid; k < L; k += F::NTH) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
+  for (int i = tid; i < L * L; i += F::NTH) {
+    const int k1 = i / L, t = i % L;
+    twN[i] = __ldg(&a.twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
+  }
+  for (int i = tid; i < H * NO; i += F::NTH) Ws[i] = __ldg(&a.W[i]);
+  __syncthreads();
+  float2* trr = tr + team * L * G::TSTR;
+  // GEMM mapping: q = tm + MT*i (i < TI), n = tn + NTg*j (j < TJ)
+  const int MT = (keep + TI - 1) / TI, NTg = (NO + TJ - 1) / TJ;
+  const bool gthread = tid < MT * NTg;
+  const int tm = tid % MT, tn = tid / MT;
+
+  for (int64_t g = blockIdx.x; g < a.G; g += gridDim.x) {
+    const int64_t bb = g / a.gx, pp = g % a.gx;
+    const float2* xg = a.x + bb * a.x_sb + pp * a.x_sp;
+    // ---- forward: rows h -> A panel
+    for (int h = team; h < H; h += TEAMS) {
+      const float2* src = xg + (int64_t)h * a.x_sh;
+      float2 v[L];
+#pragma unroll
+      for (int j = 0; j < L; ++j) v[j] = __ldg(&src[lane + L * j]);
+      wf::dftL<L, -1>(v, twL);
+#pragma unroll
+      for (int k1 = 1; k1 < L; ++k1) v[k1] = cmul(v[k1], twN[k1 * L + lane]);
+      __syncwarp(tmask);
+#pragma unroll
+      for (int k1 = 0; k1 < L; ++k1) trr[k1 * G::TSTR + lane] = v[k1];
+      __syncwarp(tmask);
+#pragma unroll
+      for (int t = 0; t < L; ++t) v[t] = trr[lane * G::TSTR + t];
+      float2 o[KP];
+      wf::dftL_first<L, KP>(v, o, twL);
+      __syncwarp(tmask);
+#pragma unroll
+      for (int k2 = 0; k2 < KP; ++k2) {
+        const int q = lane + L * k2;
+        if (q < keep) P[(size_t)h * keep + q] = o[k2];
+      }
+    }
+    __syncthreads();
+    // ---- channel mix: C[q][n] = sum_h A[h][q] W[h][n]
+    float2 acc[TI][TJ];
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    if (gthread) {
+#pragma unroll 2
+      for (int h = 0; h < H; ++h) {
+        float2 av[TI], bv[TJ];
+#pragma unroll
+        for (int i = 0; i < TI; ++i) {
+          const int q = tm + MT * i;
+          av[i] = q < keep ? P[(size_t)h * keep + q] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) {
+          const int n = tn + NTg * j;
+          bv[j] = n < NO ? Ws[h * NO + n] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+          for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+      }
+    }
+    __syncthreads();  // all A reads done before C overwrites the aliased panel
+    if (gthread) {
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) {
+        const int n = tn + NTg * j;
+#pragma unroll
+        for (int i = 0; i < TI; ++i) {
+          const int q = tm + MT * i;
+          if (q < keep && n < NO) P[(size_t)n * keep + q] = acc[i][j];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- inverse: output rows n from the C tile
+    float2* yg = a.y + bb * a.y_sb + pp * a.y_sp;
+    for (int n = team; n < NO; n += TEAMS) {
+      float2 xk[KP];
+#pragma unroll
+      for (int k2 = 0; k2 < KP; ++k2) {
+        const int q = lane + L * k2;
+        xk[k2] = q < keep ? P[(size_t)n * keep + q] : make_float2(0.f, 0.f);
+      }
+      float2 z[L];
+      wf::idftL_padded<L, KP>(xk, z, twL);
+#pragma unroll
+      for (int t = 1; t < L; ++t) z[t] = cmul(z[t], conjf2(twN[t * L + lane]));
+      __syncwarp(tmask);
+#pragma unroll
+      for (int t = 0; t < L; ++t) trr[t * G::TSTR + lane] = z[t];
+      __syncwarp(tmask);
+#pragma unroll
+      for (int k1 = 0; k1 < L; ++k1) z[k1] = trr[lane * G::TSTR + k1];
+      __syncwarp(tmask);
+      wf::dftL<L, 1>(z, twL);
+      float2* dst = yg + (int64_t)n * a.y_sn;
+#pragma unroll
+      for (int j = 0; j < L; ++j) dst[lane + L * j] = cscale(z[j], a.inv_scale);
+    }
+    __syncthreads();  // C reads done before the next item's A writes
+  }
+}
+
+bool warp_fused_supported(int n, int keep, int H, int NO) {
+  if (n != 256 && n != 1024) return false;
+  const int L = n == 256 ? 16 : 32;
+  const int kp = (keep + L - 1) / L;
+  if (kp > 8 || kp > L / 2) return false;
+  const int MT = (keep + 3) / 4, NTg = (NO + 7) / 8;
+  if (MT * NTg > 256) return false;
+  return warp_fused_smem_bytes(n, keep, H, NO) <= 220 * 1024;
+}
+
+template <int L, int KP>
+static cudaError_t launch_wfused_t(const FusedArgs& a, cudaStream_t s) {
+  const size_t smem = warp_fused_smem_bytes(L * L, a.keep, a.H, a.N);
+  cudaError_t e =
+      cudaFuncSetAttribute(warp_fused_kernel<L, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(a.G < sms ? a.G : sms);
+  warp_fused_kernel<L, KP><<<grid, 256, smem, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s) {
+  const int L = a.n == 256 ? 16 : 32;
+  const int kp = (a.keep + L - 1) / L;
+#define WFF_CASE(LL, KK) \
+  if (L == LL && kp == KK) return launch_wfused_t<LL, KK>(a, s);
+  WFF_CASE(16, 1) WFF_CASE(16, 2) WFF_CASE(16, 3) WFF_CASE(16, 4) WFF_CASE(16, 5) WFF_CASE(16, 6)
+  WFF_CASE(16, 7) WFF_CASE(16, 8)
+  WFF_CASE(32, 1) WFF_CASE(32, 2) WFF_CASE(32, 3) WFF_CASE(32, 4) WFF_CASE(32, 5) WFF_CASE(32, 6)
+  WFF_CASE(32, 7) WFF_CASE(32, 8)
+#undef WFF_CASE
+  return cudaErrorNotSupported;
+}
+
+// N = L^2 with keep (forward) / src_len (inverse) <= N/4: KP = ceil(k / L) <= L/4 <= 8
+bool warp_fft_supported(int n, int dir, int keep, int src_len) {
+  if (n != 256 && n != 1024) return false;
+  const int L = n == 256 ? 16 : 32;
+  const int k = dir < 0 ? keep : src_len;
+  if (dir < 0 && src_len != n) return false;
+  if (dir > 0 && keep != n) return false;
+  return k >= 1 && (k + L - 1) / L <= 8 && (k + L - 1) / L <= L / 2;
+}
+
+cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2* out, int64_t os, int64_t P,
+                            int keep, int src_len, float scale, const float2* tw, cudaStream_t s) {
+  const int L = n == 256 ? 16 : 32;
+  const int kp = ((dir < 0 ? keep : src_len) + L - 1) / L;
+#define WF_CASE(LL, KK)                                                                        \
+  if (L == LL && kp == KK)                                                                     \
+    return dir < 0 ? launch_wf_fwd<LL, KK>(in, is, out, os, P, keep, tw, s)                    \
+                   : launch_wf_inv<LL, KK>(in, is, out, os, P, src_len, scale, tw, s);
+  WF_CASE(16, 1) WF_CASE(16, 2) WF_CASE(16, 3) WF_CASE(16, 4) WF_CASE(16, 5) WF_CASE(16, 6) WF_CASE(16, 7)
+  WF_CASE(16, 8)
+  WF_CASE(32, 1) WF_CASE(32, 2) WF_CASE(32, 3) WF_CASE(32, 4) WF_CASE(32, 5) WF_CASE(32, 6) WF_CASE(32, 7)
+  WF_CASE(32, 8)
+#undef WF_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace tfno

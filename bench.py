@@ -424,14 +424,14 @@ def run_ours(args):
     # ---- tensor-core contraction variants of the same layer (reported, not the headline) ----
     if not args.no_baselines and prec == "fp32" and args.mode == "fully_fused":
         var = {}
-        for vp in ("tf32x3", "tf32"):
+        for vp in ("tf32x3", "tf32", "bf16"):
             try:
                 ms_v = max_over_ranks(time_steps(
                     lambda vp=vp: [T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=vp, validate=False)
                                    for _ in range(nlayers)],
                     max(3, args.steps // 2), 2, stream, barrier))
                 var[vp] = {"ms": round(ms_v, 4), "GFLOPps": round(fl["flops"] * ws / (ms_v * 1e-3) / 1e9, 2),
-                           "tolerance": 1e-5 if vp == "tf32x3" else 1e-3}
+                           "tolerance": {"tf32x3": 1e-5, "tf32": 1e-3, "bf16": 5e-3}[vp]}
             except Exception as ex:  # noqa: BLE001
                 var[vp] = {"error": str(ex)[:200]}
         T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=prec, validate=False)  # restore FP32 output
@@ -567,7 +567,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="fully_fused")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "tf32x3"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "tf32x3", "bf16"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true")

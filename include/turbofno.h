@@ -60,7 +60,7 @@ enum {
  *   FP32   FP32 SIMT CGEMM (the exact path; default)
  *   TF32   tcgen05.mma kind::tf32, one pass (stated tolerance 1e-3)
  *   TF32X3 tcgen05 3xTF32 split (hi*hi + hi*lo + lo*hi), fp32-level accuracy (1e-5)
- *   BF16   reserved (TFNO_EUNSUPPORTED in this build)
+ *   BF16   tcgen05.mma kind::f16 with bf16 operands, fp32 accumulation (stated tolerance 5e-3)
  * Only schedules with a separate contraction kernel use the tensor cores
  * (rank-2 plane path, unfused 1D); the fused row kernels always run FP32. */
 enum { TFNO_FP32 = 0, TFNO_TF32 = 1, TFNO_BF16 = 2, TFNO_TF32X3 = 3 };
@@ -129,7 +129,7 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
                int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
                int64_t c_ns, int64_t c_bs, float alpha, void* stream);
 
-/* tfno_cgemm with a contraction precision (TFNO_FP32 / TFNO_TF32 / TFNO_TF32X3).
+/* tfno_cgemm with a contraction precision (TFNO_FP32 / TFNO_TF32 / TFNO_TF32X3 / TFNO_BF16).
  * The tensor-core path needs the mode layout: a_ms = c_ms = w_ns = 1, w_bs = 0 (N > 128 runs in
  * 128-channel blocks). */
 int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, int64_t a_ms, int64_t a_ks,

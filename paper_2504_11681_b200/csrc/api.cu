@@ -467,7 +467,7 @@ int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* 
                     int64_t c_ns, int64_t c_bs, float alpha, int prec, void* stream) {
   if (prec == TFNO_FP32)
     return tfno_cgemm(M, N, K, batch, A, a_ms, a_ks, a_bs, W, w_ks, w_ns, w_bs, C, c_ms, c_ns, c_bs, alpha, stream);
-  if (prec != TFNO_TF32 && prec != TFNO_TF32X3) return TFNO_EUNSUPPORTED;
+  if (prec != TFNO_TF32 && prec != TFNO_TF32X3 && prec != TFNO_BF16) return TFNO_EUNSUPPORTED;
   if (M < 0 || N < 0 || K < 0 || batch < 0) return TFNO_EINVAL;
   if (M == 0 || N == 0 || batch == 0) return TFNO_OK;
   if (!A || !W || !C) return TFNO_EINVAL;
@@ -553,7 +553,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
                        void* wsv, size_t ws_bytes, void* stream) {
   if (!c || mode < TFNO_STAGED || mode > TFNO_FULLY_FUSED) return TFNO_EINVAL;
   if (tfno_config_violations(c, nullptr, 8)) return TFNO_EINVAL;
-  if (prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3) return prec == TFNO_BF16 ? TFNO_EUNSUPPORTED : TFNO_EINVAL;
+  if (prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3 && prec != TFNO_BF16) return TFNO_EINVAL;
   if (!xv || !wv || !yv) return TFNO_EINVAL;
   if (c->dim_x > TFNO_TW_MAX || c->dim_y > TFNO_TW_MAX) return TFNO_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -43,6 +44,23 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint3
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool kmajor) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((kmajor ? 0u : 1u) << 15) | ((kmajor ? 0u : 1u) << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// kind::f16 with BF16 operands (format 1), D f32, K-major
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -289,6 +307,168 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
 }
 
+// ---------------------------------------------------------------- BF16 variant
+// Same structure; kind::f16 with bf16 operands: K = 16 per MMA, K-major core
+// matrix = 8 rows x 8 bf16 (16 B), LBO between groups of 8 K.  A item (m, quad
+// of 4 channels) = one 16-byte row (re/im of 4 channels); B item (n, quad)
+// = rows 2n (Wr, -Wi, ...) and 2n+1 (Wi, Wr, ...).
+__device__ __forceinline__ uint32_t cm_off16(int mn, int k, int lbo) {
+  return (uint32_t)((k >> 3) * lbo + (mn >> 3) * 128 + (mn & 7) * 16 + (k & 7) * 2);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(128, 1) cgemm_tc_bf16_kernel(GemmArgs g) {
+  using Gm = TcGeo<NP>;
+  constexpr int A_TILE = TC_BM * TC_BK * 2, B_TILE = NP * TC_BK * 2;
+  constexpr int A_LBO = (TC_BM / 8) * 128, B_LBO = (NP / 8) * 128;
+  constexpr int STAGE = A_TILE + B_TILE;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = g.M, N = g.N, K = g.K;
+  const int mtiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));
+  const int64_t tiles = (int64_t)mtiles * nsplit * g.batch;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);
+  if (tid == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::saddr(tmem_slot)),
+                 "n"(Gm::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t IDESC = tc::make_idesc_bf16(TC_BM, NP);
+  constexpr int AI = TC_BM * 4 / 128, BI = (NP / 2) * 4 / 128;  // items per thread
+  uint4 ra[AI], rb0[BI], rb1[BI];
+
+  auto load_chunk = [&](int64_t tile, int c) {
+    const int64_t b = tile / ((int64_t)mtiles * nsplit);
+    const int64_t m0 = (tile % mtiles) * TC_BM;
+    const int64_t n0 = ((tile / mtiles) % nsplit) * (NP / 2);
+    const int64_t h0 = (int64_t)c * (TC_BK / 2);
+    const float2* Ab = g.A + b * g.a_bs;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 128;
+      const int ml = idx % TC_BM, hq = idx / TC_BM;
+      const int64_t m = m0 + ml, h = h0 + 4 * hq;
+      float2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (m < M && h + q < K) ? __ldg(Ab + (h + q) * g.a_ks + m) : make_float2(0.f, 0.f);
+      ra[i] = make_uint4(tc::pack_bf16(v[0].x, v[0].y), tc::pack_bf16(v[1].x, v[1].y), tc::pack_bf16(v[2].x, v[2].y),
+                         tc::pack_bf16(v[3].x, v[3].y));
+    }
+#pragma unroll
+    for (int i = 0; i < BI; ++i) {
+      const int idx = tid + i * 128;
+      const int nl = idx % (NP / 2), hq = idx / (NP / 2);
+      const int64_t h = h0 + 4 * hq, n = n0 + nl;
+      float2 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = (n < N && h + q < K) ? __ldg(g.W + (h + q) * g.w_ks + n) : make_float2(0.f, 0.f);
+      rb0[i] = make_uint4(tc::pack_bf16(w[0].x, -w[0].y), tc::pack_bf16(w[1].x, -w[1].y),
+                          tc::pack_bf16(w[2].x, -w[2].y), tc::pack_bf16(w[3].x, -w[3].y));
+      rb1[i] = make_uint4(tc::pack_bf16(w[0].y, w[0].x), tc::pack_bf16(w[1].y, w[1].x),
+                          tc::pack_bf16(w[2].y, w[2].x), tc::pack_bf16(w[3].y, w[3].x));
+    }
+  };
+  auto store_chunk = [&](int st) {
+    uint8_t* sA = stage_base + st * STAGE;
+    uint8_t* sB = sA + A_TILE;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 128;
+      const int ml = idx % TC_BM, hq = idx / TC_BM;
+      *reinterpret_cast<uint4*>(sA + cm_off16(ml, 8 * hq, A_LBO)) = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BI; ++i) {
+      const int idx = tid + i * 128;
+      const int nl = idx % (NP / 2), hq = idx / (NP / 2);
+      *reinterpret_cast<uint4*>(sB + cm_off16(2 * nl, 8 * hq, B_LBO)) = rb0[i];
+      *reinterpret_cast<uint4*>(sB + cm_off16(2 * nl + 1, 8 * hq, B_LBO)) = rb1[i];
+    }
+  };
+
+  int64_t gch = 0;
+  int64_t tile = blockIdx.x;
+  if (tile < tiles) load_chunk(tile, 0);
+  for (; tile < tiles; tile += gridDim.x) {
+    for (int c = 0; c < nchunks; ++c, ++gch) {
+      const int st = (int)(gch & 1);
+      if (gch >= 2) tc::mbar_wait(&bars[st], (uint32_t)(((gch - 2) >> 1) & 1));
+      store_chunk(st);
+      if (c + 1 < nchunks)
+        load_chunk(tile, c + 1);
+      else if (tile + gridDim.x < tiles)
+        load_chunk(tile + gridDim.x, 0);
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        const uint32_t a0 = tc::saddr(stage_base + st * STAGE), b0 = a0 + A_TILE;
+#pragma unroll
+        for (int s = 0; s < TC_BK / 16; ++s) {  // K = 16 per MMA = 2 K groups of 8
+          const uint64_t ad = tc::make_desc(a0 + 2 * s * A_LBO, A_LBO, 128);
+          const uint64_t bd = tc::make_desc(b0 + 2 * s * B_LBO, B_LBO, 128);
+          tc::mma_bf16(tmem, ad, bd, IDESC, (c > 0 || s > 0) ? 1u : 0u);
+        }
+        tc::commit(&bars[st]);
+      }
+    }
+    {
+      const int64_t last = gch - 1;
+      tc::mbar_wait(&bars[last & 1], (uint32_t)((last >> 1) & 1));
+      tc::fence_after();
+      const int64_t b = tile / ((int64_t)mtiles * nsplit);
+      const int64_t n0 = ((tile / mtiles) % nsplit) * (NP / 2);
+      const int64_t m = (tile % mtiles) * TC_BM + warp * 32 + lane;
+      float2* Cb = g.C + b * g.c_bs;
+#pragma unroll 1
+      for (int col = 0; col < NP; col += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + col, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t n = n0 + col / 2 + q;
+          if (m < M && n < N) Cb[n * g.c_ns + m] = make_float2(g.alpha * v[2 * q], g.alpha * v[2 * q + 1]);
+        }
+      }
+      tc::fence_before();
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
+}
+
+template <int NP>
+static cudaError_t launch_tc_bf16_t(const GemmArgs& g, cudaStream_t s) {
+  const size_t smem = 2 * (TC_BM * TC_BK * 2 + NP * TC_BK * 2) + 64;
+  cudaError_t e =
+      cudaFuncSetAttribute(cgemm_tc_bf16_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * ((g.N + NP / 2 - 1) / (NP / 2)) * g.batch;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  cgemm_tc_bf16_kernel<NP><<<grid, 128, smem, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 template <int NP, int PASSES>
 static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
   constexpr int STAGE = (PASSES > 1 ? 2 : 1) * (TcGeo<NP>::A_TILE + TcGeo<NP>::B_TILE);
@@ -316,6 +496,11 @@ bool cgemm_tc_supported(const GemmArgs& g) {
 cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s) {
   if (!cgemm_tc_supported(g)) return cudaErrorNotSupported;
   const int np = (int)(2 * g.N);
+  if (passes == 0) {  // BF16 operands
+    if (np <= 64) return launch_tc_bf16_t<64>(g, s);
+    if (np <= 128) return launch_tc_bf16_t<128>(g, s);
+    return launch_tc_bf16_t<256>(g, s);
+  }
   if (passes == 1) {
     if (np <= 64) return launch_tc_t<64, 1>(g, s);
     if (np <= 128) return launch_tc_t<128, 1>(g, s);

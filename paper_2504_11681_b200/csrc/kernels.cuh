@@ -61,10 +61,12 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s);
 // tcgen05 TF32 contraction (cgemm_tc.cu): passes 1 = TF32, 3 = 3xTF32 (fp32-level accuracy)
 bool cgemm_tc_supported(const GemmArgs& g);
 cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s);
-// precision dispatch: 0 FP32 SIMT, 1 TF32 tcgen05, 3 3xTF32 tcgen05
+// precision dispatch: 0 FP32 SIMT, 1 TF32 tcgen05, 2 BF16 tcgen05, 3 3xTF32 tcgen05
+// (launch_cgemm_tc passes: 1 TF32, 3 3xTF32, 0 BF16)
 inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s) {
   if (prec == 0) return launch_cgemm(g, s);
   if (prec == 1 || prec == 3) return launch_cgemm_tc(g, prec == 1 ? 1 : 3, s);
+  if (prec == 2) return launch_cgemm_tc(g, 0, s);
   return cudaErrorNotSupported;
 }
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);

@@ -97,6 +97,10 @@ __device__ __forceinline__ void idftL_padded(const float2* x, float2* out, const
 
 }  // namespace wf
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 template <int L>
 struct WfGeo {
   static constexpr int N = L * L;
@@ -421,8 +425,187 @@ cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s) {
   return cudaErrorNotSupported;
 }
 
+// ---------------------------------------------------------------- team FFTs, N = 1024*U
+// A team of T = 32*U threads per row (U = 2: N = 2048, U = 4: N = 4096), 32
+// register values per thread, n = t + T*j:
+//   forward  stage 1: DFT32 over j (registers), twiddle w_N^{t k1}; transpose
+//            [k1][t] through smem; stage 2: X[k1 + 32 k2] = sum_t w_T^{t k2} Y_t[k1]
+//            with t = u + U*s: thread (k1, u) runs DFT32 over s, twiddles by
+//            w_T^{u k2}, and the U partial sums of its k1 are reduced across the
+//            U adjacent lanes with shuffles (first K2 = ceil(keep/32) outputs).
+//   inverse  thread (k1, u): padded DFT32 over k2 of X[k1 + 32 k2] w_T^{+k2 u}
+//            gives z[u + U s]; twiddle w_N^{+k1 t}; transpose [t][k1];
+//            thread t: DFT32 over k1 -> y[t + T j].  No cross-lane reduction.
+template <int U>
+struct TfGeo {
+  static constexpr int T = 32 * U, N = 32 * T, NTH = 512, TEAMS = NTH / T;
+  static constexpr int TSTR = 33;  // padded transpose stride
+  static constexpr size_t smem_bytes() {
+    return sizeof(float2) * ((size_t)32 + (size_t)32 * T + (size_t)TEAMS * T * TSTR + (size_t)T);
+  }
+};
+
+template <int U, int K2>
+__global__ void __launch_bounds__(512, 1) team_fft_fwd_kernel(const float2* __restrict__ in, int64_t in_stride,
+                                                            float2* __restrict__ out, int64_t out_stride, int64_t P,
+                                                            int keep, const float2* __restrict__ twg) {
+  using G = TfGeo<U>;
+  constexpr int T = G::T, N = G::N;
+  extern __shared__ __align__(16) float2 sm[];
+  float2* tw32 = sm;                  // w_32^k
+  float2* twN = tw32 + 32;            // [k1][t] = w_N^{t k1}, k1 < 32, t < T
+  float2* tr = twN + 32 * T;          // TEAMS x T x TSTR
+  float2* twT = tr + G::TEAMS * T * G::TSTR;  // w_T^k
+  const int tid = threadIdx.x, team = tid / T, tt = tid % T;
+  for (int k = tid; k < 32; k += G::NTH) tw32[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / 32)]);
+  for (int k = tid; k < T; k += G::NTH) twT[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / T)]);
+  for (int i = tid; i < 32 * T; i += G::NTH) {
+    const int k1 = i / T, t = i % T;
+    twN[i] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
+  }
+  __syncthreads();
+  float2* trr = tr + team * T * G::TSTR;
+  const int k1s = tt / U, us = tt % U;  // stage-2 role
+  for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS) {
+    const int64_t row = row0 + team;
+    const bool live = row < P;
+    float2 v[32];
+    const float2* src = in + (live ? row : 0) * in_stride;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = live ? __ldg(&src[tt + T * j]) : make_float2(0.f, 0.f);
+    wf::dftL<32, -1>(v, tw32);
+#pragma unroll
+    for (int k1 = 1; k1 < 32; ++k1) v[k1] = cmul(v[k1], twN[k1 * T + tt]);
+    named_bar_sync(1 + team, T);
+#pragma unroll
+    for (int k1 = 0; k1 < 32; ++k1) trr[tt * G::TSTR + k1] = v[k1];  // [t][k1]
+    named_bar_sync(1 + team, T);
+    // thread (k1s, us): Y_{us + U s}[k1s] for s < 32
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = trr[(us + U * s2) * G::TSTR + k1s];
+    wf::dftL<32, -1>(v, tw32);  // V_u[k2'] over s
+    float2 o[K2];
+#pragma unroll
+    for (int k2 = 0; k2 < K2; ++k2) o[k2] = (us && k2) ? cmul(v[k2], twT[(us * k2) % T]) : v[k2];
+    // sum over the U adjacent lanes (u)
+#pragma unroll
+    for (int m = 1; m < U; m <<= 1)
+#pragma unroll
+      for (int k2 = 0; k2 < K2; ++k2) {
+        float2 p;
+        p.x = __shfl_xor_sync(0xffffffffu, o[k2].x, m);
+        p.y = __shfl_xor_sync(0xffffffffu, o[k2].y, m);
+        o[k2] = cadd(o[k2], p);
+      }
+    if (live) {
+      float2* dst = out + row * out_stride;
+#pragma unroll
+      for (int k2 = 0; k2 < K2; ++k2) {
+        if (k2 % U != us) continue;  // lanes of a k1 group split the stores
+        const int k = k1s + 32 * k2;
+        if (k < keep) dst[k] = o[k2];
+      }
+    }
+    named_bar_sync(1 + team, T);
+  }
+}
+
+template <int U, int K2>
+__global__ void __launch_bounds__(512, 1) team_fft_inv_kernel(const float2* __restrict__ in, int64_t in_stride,
+                                                            float2* __restrict__ out, int64_t out_stride, int64_t P,
+                                                            int src_len, float scale,
+                                                            const float2* __restrict__ twg) {
+  using G = TfGeo<U>;
+  constexpr int T = G::T, N = G::N;
+  extern __shared__ __align__(16) float2 sm[];
+  float2* tw32 = sm;
+  float2* twN = tw32 + 32;
+  float2* tr = twN + 32 * T;
+  float2* twT = tr + G::TEAMS * T * G::TSTR;
+  const int tid = threadIdx.x, team = tid / T, tt = tid % T;
+  for (int k = tid; k < 32; k += G::NTH) tw32[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / 32)]);
+  for (int k = tid; k < T; k += G::NTH) twT[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / T)]);
+  for (int i = tid; i < 32 * T; i += G::NTH) {
+    const int k1 = i / T, t = i % T;
+    twN[i] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
+  }
+  __syncthreads();
+  float2* trr = tr + team * T * G::TSTR;
+  const int k1s = tt / U, us = tt % U;
+  for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS) {
+    const int64_t row = row0 + team;
+    const bool live = row < P;
+    const float2* src = in + (live ? row : 0) * in_stride;
+    // thread (k1s, us): inputs X[k1s + 32 k2] w_T^{+k2 us}, padded DFT32 over k2 -> s
+    float2 z[32];
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) {
+      if (k2 < K2) {
+        const int k = k1s + 32 * k2;
+        float2 xv = (live && k < src_len) ? __ldg(&src[k]) : make_float2(0.f, 0.f);
+        z[k2] = (us && k2) ? cmul(xv, conjf2(twT[(us * k2) % T])) : xv;
+      } else {
+        z[k2] = make_float2(0.f, 0.f);
+      }
+    }
+    wf::dftL<32, 1>(z, tw32);  // z[s] -> value at t = us + U s
+    named_bar_sync(1 + team, T);
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) {
+      const int t = us + U * s2;
+      trr[t * G::TSTR + k1s] = cmul(z[s2], conjf2(twN[k1s * T + t]));  // w_N^{+k1 t}
+    }
+    named_bar_sync(1 + team, T);
+    // thread t: DFT32 over k1 -> y[t + T j]
+#pragma unroll
+    for (int k1 = 0; k1 < 32; ++k1) z[k1] = trr[tt * G::TSTR + k1];
+    wf::dftL<32, 1>(z, tw32);
+    if (live) {
+      float2* dst = out + row * out_stride;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) dst[tt + T * j] = cscale(z[j], scale);
+    }
+    named_bar_sync(1 + team, T);
+  }
+}
+
+template <int U, int K2>
+static cudaError_t launch_tf(int dir, const float2* in, int64_t is, float2* out, int64_t os, int64_t P, int keep,
+                             int src_len, float scale, const float2* tw, cudaStream_t s) {
+  using G = TfGeo<U>;
+  const size_t smem = G::smem_bytes();
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (P + G::TEAMS - 1) / G::TEAMS;
+  const int grid = (int)(blocks < (int64_t)sms ? blocks : (int64_t)sms);
+  cudaError_t e;
+  if (dir < 0) {
+    e = cudaFuncSetAttribute(team_fft_fwd_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    team_fft_fwd_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw);
+  } else {
+    e = cudaFuncSetAttribute(team_fft_inv_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    team_fft_inv_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, src_len, scale, tw);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // N = L^2 with keep (forward) / src_len (inverse) <= N/4: KP = ceil(k / L) <= L/4 <= 8
+static int team_k2(int k) {  // K2 template bucket for the team kernels
+  const int k2 = (k + 31) / 32;
+  return k2 <= 4 ? 4 : k2 <= 8 ? 8 : k2 <= 16 ? 16 : 32;
+}
+
 bool warp_fft_supported(int n, int dir, int keep, int src_len) {
+  if (n == 2048 || n == 4096) {
+    if (dir < 0 && src_len != n) return false;
+    if (dir > 0 && keep != n) return false;
+    const int k = dir < 0 ? keep : src_len;
+    return k >= 1 && (k + 31) / 32 <= 32;
+  }
   if (n != 256 && n != 1024) return false;
   const int L = n == 256 ? 16 : 32;
   const int k = dir < 0 ? keep : src_len;
@@ -433,6 +616,15 @@ bool warp_fft_supported(int n, int dir, int keep, int src_len) {
 
 cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2* out, int64_t os, int64_t P,
                             int keep, int src_len, float scale, const float2* tw, cudaStream_t s) {
+  if (n == 2048 || n == 4096) {
+    const int kb = team_k2(dir < 0 ? keep : src_len);
+#define TF_CASE(UU, KK) \
+  if (n == 1024 * UU && kb == KK) return launch_tf<UU, KK>(dir, in, is, out, os, P, keep, src_len, scale, tw, s);
+    TF_CASE(2, 4) TF_CASE(2, 8) TF_CASE(2, 16) TF_CASE(2, 32) TF_CASE(4, 4) TF_CASE(4, 8) TF_CASE(4, 16)
+    TF_CASE(4, 32)
+#undef TF_CASE
+    return cudaErrorNotSupported;
+  }
   const int L = n == 256 ? 16 : 32;
   const int kp = ((dir < 0 ? keep : src_len) + L - 1) / L;
 #define WF_CASE(LL, KK)                                                                        \

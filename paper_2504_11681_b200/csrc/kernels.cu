@@ -179,9 +179,15 @@ __global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
   const int tid = threadIdx.x;
   const int tm = tid % 16, tn = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
-  const int64_t b = blockIdx.z;
+  // fold > 1: the tile spans `fold` batch elements of M (< FBM) modes each
+  const int64_t fold = g.fold > 1 ? g.fold : 1;
+  const int64_t b = blockIdx.z * fold;
   const float2* __restrict__ A = g.A + b * g.a_bs;
-  const float2* __restrict__ W = g.W + b * g.w_bs;
+  const float2* __restrict__ W = g.W + (fold > 1 ? 0 : b * g.w_bs);
+  auto a_off = [&](int64_t gm) -> int64_t {  // tile-local m -> element offset (batch folded)
+    return fold > 1 ? (gm / g.M) * g.a_bs + gm % g.M : gm;
+  };
+  auto m_ok = [&](int64_t gm) { return fold > 1 ? (gm / g.M < fold && b + gm / g.M < g.batch) : gm < g.M; };
   // loader mapping: A chunk = FBK x FBM complex = 512 float4 (2 / thread),
   //                 W chunk = FBK x FBN complex = 1024 float4 (4 / thread)
   constexpr int NA = FBK * FBM / 2 / 256, NW = FBK * FBN / 2 / 256;  // float4 per thread
@@ -192,7 +198,10 @@ __global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
       const int i = tid + r * 256;
       const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
       const int64_t gk = k0 + kk, gm = m0 + mm;
-      if (gk < g.K && gm + 1 < g.M) {
+      if (fold > 1) {  // M even: the pair (gm, gm+1) stays inside one batch element
+        ra[r] = (gk < g.K && m_ok(gm)) ? __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + a_off(gm)))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (gk < g.K && gm + 1 < g.M) {
         ra[r] = __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + gm));
       } else {
         float2 v0 = (gk < g.K && gm < g.M) ? A[gk * g.a_ks + gm] : make_float2(0.f, 0.f);
@@ -262,7 +271,11 @@ __global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
 #pragma unroll
     for (int i = 0; i < TI; ++i) {
       const int64_t gm = m0 + tm + 16 * i;
-      if (gm < g.M) C[gn * g.c_ns + gm] = cscale(acc[i][j], g.alpha);
+      if (fold > 1) {
+        if (m_ok(gm)) C[(gm / g.M) * g.c_bs + gn * g.c_ns + gm % g.M] = cscale(acc[i][j], g.alpha);
+      } else if (gm < g.M) {
+        C[gn * g.c_ns + gm] = cscale(acc[i][j], g.alpha);
+      }
     }
   }
 }
@@ -271,7 +284,16 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   const bool fast = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) &&
                     (g.w_ks % 2 == 0) && (g.w_bs % 2 == 0) && g.N > 16 && g.M >= 64 &&
                     ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0);
-  if (fast && g.N > 64) {
+  // small M (1D modes): fold batch elements into the 64-row tile
+  const bool foldable = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.M >= 2 && g.M < 64 &&
+                        (64 % g.M == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) && (g.w_ks % 2 == 0) &&
+                        ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0) && g.N > 16;
+  if (foldable) {
+    GemmArgs f = g;
+    f.fold = 64 / g.M;
+    dim3 grid(1u, (unsigned)((g.N + 127) / 128), (unsigned)((g.batch + f.fold - 1) / f.fold));
+    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(f);
+  } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);
   } else if (fast && g.M >= 128) {

@@ -31,6 +31,7 @@ struct GemmArgs {
   float2* C;
   int64_t c_ms, c_ns, c_bs;
   float alpha;
+  int64_t fold;  // batch elements folded into one M tile (0/1 = none; mode-layout fast path only)
 };
 
 // Row-fused layer kernel (FFT along contiguous rows -> CGEMM over the

@@ -16,9 +16,9 @@ def env():
     return T, O, torch
 
 
-@pytest.mark.parametrize("M,N,K,B", [(4096, 128, 128, 2), (512, 256, 256, 2), (200, 300, 40, 1), (1024, 64, 64, 3), (256, 64, 64, 2), (300, 37, 20, 2),
+@pytest.mark.parametrize("M,N,K,B", [(4096, 128, 128, 2), (512, 256, 256, 2), (200, 300, 40, 1), (1024, 64, 64, 3), (256, 64, 64, 2), (300, 37, 20, 2), (32, 64, 64, 5), (16, 40, 30, 7), (32, 256, 256, 3),
                                      (32, 64, 64, 4), (129, 1, 3, 1), (128, 128, 256, 1)])
-@pytest.mark.parametrize("prec,tol", [("tf32x3", 1e-5), ("tf32", 2e-3), ("bf16", 1e-2)])
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("tf32x3", 1e-5), ("tf32", 2e-3), ("bf16", 1e-2)])
 def test_tc_cgemm_vs_float64(env, M, N, K, B, prec, tol):
     T, O, torch = env
     rng = np.random.default_rng(M + N + K)

@@ -1,0 +1,43 @@
+"""Small invocations of every kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck):  tools/sanitize.sh"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2504_11681_b200 as T  # noqa: E402
+from paper_2504_11681_b200 import multigpu as MG  # noqa: E402
+
+dev = torch.device("cuda:0")
+rng = np.random.default_rng(0)
+
+
+def rnd(*shape):
+    return torch.from_numpy((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64)).to(dev)
+
+
+cases = [((1, 2, 2, 128, 128, 16, 16, 2), ["fully_fused"]),            # plane2d G128
+         ((1, 1, 1, 512, 512, 64, 64, 2), ["fully_fused"]),            # plane2d G512 (TMA ring, producer warp)
+         ((2, 3, 2, 32, 64, 8, 16, 2), list(T.MODES)),                  # paper schedule + generic kernels
+         ((2, 8, 8, 1, 1024, 1, 128, 1), ["fully_fused", "fft_optimized"]),  # warp fused / warp rows
+         ((3, 8, 8, 1, 256, 1, 32, 1), ["fully_fused", "fft_optimized"]),
+         ((1, 4, 4, 1, 4096, 1, 512, 1), ["fully_fused"]),               # team rows
+         ((2, 8, 8, 1, 128, 1, 32, 1), ["fully_fused", "fused_fft_gemm", "fused_gemm_ifft"])]  # CT rows fused
+for shape, modes in cases:
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = rnd(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), rnd(cfg.hidden_dim, cfg.output_dim)
+    for mode in modes:
+        T.run_layer_device(cfg, x, w, mode=mode)
+        torch.cuda.synchronize()
+        print("ok", shape, mode, flush=True)
+for prec in ("tf32", "tf32x3", "bf16"):
+    A = rnd(2, 64, 256).transpose(1, 2)
+    T.cgemm_device(A, rnd(64, 96), precision=prec)
+    torch.cuda.synchronize()
+    print("ok cgemm", prec, flush=True)
+cfg = T.FnoLayerConfig(1, 4, 4, 256, 256, 32, 32, 2)
+MG.spectrum_inverse(cfg, MG.spectrum_forward(cfg, rnd(1, 4, 256, 256)), (1, 4))
+torch.cuda.synchronize()
+print("ok spectrum")

@@ -209,8 +209,12 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   for (int r = 0; r < 8; ++r) tw1[r] = twy[r * tt];
 #pragma unroll
   for (int t = 0; t < 8; ++t) tw2[t] = twy[(8 * t * a_) % NY];
-  // reduction reader role: output storage column q' = tt = t' + T*r'
+  // reduction reader role: output storage column q' = tt = t' + T*r'; its
+  // twiddles w_M^{tq*a} are applied inside the sum (complex FMAs)
   const int tq = tt % T, rq = tt / T;
+  float2 tw3[A];
+#pragma unroll
+  for (int a = 0; a < A; ++a) tw3[a] = twy[(8 * tq * a) % NY];
 
   float2 acc[G::TASKS2][KA];
 #pragma unroll
@@ -242,9 +246,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
       float2 u[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) u[c] = trt[r_ * TS + a_ + A * c];
-      dft8<-1>(u);
-#pragma unroll
-      for (int t = 1; t < T; ++t) u[t] = cmul(u[t], tw2[t]);
+      dft8<-1>(u);  // twiddle w_M^{t a} deferred to the reduction (FMA-fused)
       float2* dst = redt + r_ * RS + a_ * RT;
       if constexpr (T % 2 == 0) {
 #pragma unroll
@@ -261,11 +263,16 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
       float2 part[A];
 #pragma unroll
       for (int a = 0; a < A; ++a) part[a] = redt[rq * RS + a * RT + tq];
+      // sum_a w_M^{tq a} part[a]: two interleaved FMA chains, then one add
+      float2 s0 = part[0], s1 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int w = 1; w < A; w *= 2)  // tree: log2(A) dependent adds instead of A-1
-#pragma unroll
-        for (int a = 0; a < A; a += 2 * w) part[a] = cadd(part[a], part[a + w]);
-      const float2 sacc = part[0];
+      for (int a = 1; a < A; ++a) {
+        if (a & 1)
+          cmac(s1, part[a], tw3[a]);
+        else
+          cmac(s0, part[a], tw3[a]);
+      }
+      const float2 sacc = cadd(s0, s1);
       const int x1 = j * TEAMS + team;
       Tc[x1 * KY + tt] = sacc;
     }

@@ -26,6 +26,7 @@
 // Z[y1, r] = sum_{y2} w_8^{r y2} x[y1 + M y2], M = N/8, A = M/8.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -144,7 +145,7 @@ constexpr int kComputeBar = 15;
 // Warp-specialised: warp NTH/32 is the TMA producer (ring of S slots, full /
 // empty mbarriers); the NTH compute threads form row teams that synchronise
 // only inside the team, plus one compute-wide barrier per class (column pass).
-template <class G, int S, bool NATURAL>
+template <class G, int S, bool NATURAL, bool DLD>
 __global__ void __launch_bounds__(G::NTH + 32, 1)
     plane_fwd2d_kernel(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes,
                        const float2* __restrict__ twg) {
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   constexpr int RT = G::RT, RS = G::RS;
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);
-  float2* tr = ring + S * TEAMS * NY;
+  float2* tr = ring + (DLD ? 0 : S * TEAMS * NY);  // DLD: rows go straight to registers (no ring)
   float2* red = tr + TEAMS * 8 * TS;
   float2* Tc = red + TEAMS * 8 * RS;
   float2* twy = Tc + KX * KY;
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
 
   if (tid >= NTH) {
     // ---------------- producer warp: stream the plane rows, class by class
-    if (tid == NTH) {
+    if (!DLD && tid == NTH) {
       const uint64_t pol = policy_evict_first();
       for (int64_t it = 0; it < NIT; ++it) {
         const int slot = (int)(it % S);
@@ -222,19 +223,43 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
 #pragma unroll
     for (int u = 0; u < KA; ++u) acc[a][u] = make_float2(0.f, 0.f);
 
+  // DLD: this thread's 8 inputs of the next iteration's row, loaded one iteration ahead
+  auto row_ptr = [&](int64_t it2) {
+    const int64_t pl = blockIdx.x + (it2 / (R * IPC)) * gridDim.x;
+    const int xx0 = (int)((it2 / IPC) % R), jj = (int)(it2 % IPC);
+    return x + pl * (int64_t)DX * NY + (int64_t)(xx0 + R * (jj * TEAMS + team)) * NY;
+  };
+  float2 nxt[8];
+  if (DLD && NIT > 0) {
+    const float2* rp = row_ptr(0);
+#pragma unroll
+    for (int y2 = 0; y2 < 8; ++y2) nxt[y2] = __ldcs(rp + tt + M * y2);
+  }
   for (int64_t it = 0; it < NIT; ++it) {
     const int slot = (int)(it % S);
     const int x0 = (int)((it / IPC) % R), j = (int)(it % IPC);
-    mbar_wait(&full[slot], (uint32_t)((it / S) & 1));
+    if (!DLD) mbar_wait(&full[slot], (uint32_t)((it / S) & 1));
     // ---- row stage 1: radix-8 over y2, twiddle w_N^{r*y1}, transpose
     {
-      const float2* row = ring + slot * TEAMS * NY + team * NY;
       float2 v[8];
+      if (DLD) {
 #pragma unroll
-      for (int y2 = 0; y2 < 8; ++y2) v[y2] = row[tt + M * y2];
+        for (int y2 = 0; y2 < 8; ++y2) v[y2] = nxt[y2];
+        if (it + 1 < NIT) {
+          const float2* rp = row_ptr(it + 1);
+#pragma unroll
+          for (int y2 = 0; y2 < 8; ++y2) nxt[y2] = __ldcs(rp + tt + M * y2);
+        }
+      } else {
+        const float2* row = ring + slot * TEAMS * NY + team * NY;
+#pragma unroll
+        for (int y2 = 0; y2 < 8; ++y2) v[y2] = row[tt + M * y2];
+      }
       dft8<-1>(v);
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+      if (!DLD) {
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+      }
 #pragma unroll
       for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
 #pragma unroll
@@ -332,15 +357,15 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
 // ============================================================== inverse
 // Row teams run decoupled (team barriers only); each team's elected thread
 // TMA-stores its own finished rows from a per-team staging ring.
-template <class G, int SO, bool NATURAL>
+template <class G, int SO, bool NATURAL, bool DST>
 __global__ void __launch_bounds__(G::NTH, 1)
     plane_inv2d_kernel(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes,
                        const float2* __restrict__ twg, float scale) {
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
   extern __shared__ __align__(128) uint8_t smem[];
-  float2* ost = reinterpret_cast<float2*>(smem);  // TEAMS x SO x NY (TMA store sources)
-  float2* cin = ost + TEAMS * SO * NY;            // KX*KY (TMA load target)
+  float2* ost = reinterpret_cast<float2*>(smem);  // TEAMS x SO x NY (TMA store sources; unused if DST)
+  float2* cin = ost + (DST ? 0 : TEAMS * SO * NY);  // KX*KY (TMA load target)
   float2* Gb = cin + KX * KY;                     // KX*KY
   float2* tr = Gb + KX * KY;
   float2* twy = tr + TEAMS * 8 * TS;
@@ -430,7 +455,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
           for (int c = 0; c < 8; ++c) trt[r_ * TS + a_ + A * c] = u[c];
         }
         const int slot = (int)(gi % SO);
-        if (elected) bulk_wait_read<SO - 1>();  // staging slot free again
+        if (!DST && elected) bulk_wait_read<SO - 1>();  // staging slot free again
         team_sync<M>(team);
         // ---- row stage B: twiddle w_N^{+r y1}, radix 8 over r -> staging row
         {
@@ -440,13 +465,19 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
           for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
           dft8<1>(v);
-          float2* o = ostt + slot * NY;
+          if (DST) {  // coalesced streaming stores straight from registers (no smem staging)
+            float2* orow = yp + (int64_t)(x0 + R * x1) * NY;
 #pragma unroll
-          for (int y2 = 0; y2 < 8; ++y2) o[tt + M * y2] = v[y2];
+            for (int y2 = 0; y2 < 8; ++y2) __stcs(orow + tt + M * y2, v[y2]);
+          } else {
+            float2* o = ostt + slot * NY;
+#pragma unroll
+            for (int y2 = 0; y2 < 8; ++y2) o[tt + M * y2] = v[y2];
+          }
         }
-        fence_proxy_async();
+        if (!DST) fence_proxy_async();
         team_sync<M>(team);
-        if (elected) {
+        if (!DST && elected) {
           const int row = x0 + R * x1;
           tma_store_1d(yp + (int64_t)row * NY, ostt + slot * NY, NY * 8, pol);
           bulk_commit();
@@ -454,21 +485,40 @@ __global__ void __launch_bounds__(G::NTH, 1)
       }
     }
   }
-  if (elected) bulk_wait_all();
+  if (!DST && elected) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- dispatch
 template <class G>
-constexpr size_t fwd_smem(int S) {
-  return sizeof(float2) * ((size_t)S * G::TEAMS * G::NY + G::TEAMS * 8 * (G::TS + G::RS) + G::KX * G::KY +
-                           G::NY + G::DX) +
+constexpr size_t fwd_smem(int S, bool dld = false) {
+  return sizeof(float2) * ((size_t)(dld ? 0 : S) * G::TEAMS * G::NY + G::TEAMS * 8 * (G::TS + G::RS) +
+                           G::KX * G::KY + G::NY + G::DX) +
          16 * S + 64;
 }
 template <class G>
-constexpr size_t inv_smem(int SO) {
-  return sizeof(float2) * (2 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS + (size_t)SO * G::TEAMS * G::NY +
-                           G::NY + G::DX) +
+constexpr size_t inv_smem(int SO, bool dst = false) {
+  return sizeof(float2) * (2 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS +
+                           (size_t)(dst ? 0 : SO) * G::TEAMS * G::NY + G::NY + G::DX) +
          16 + 64;
+}
+
+// HBM-side data paths per geometry (bit0 = inverse stores rows straight from
+// registers with st.global.cs, else smem staging + TMA bulk store; bit1 =
+// forward loads rows straight into registers one iteration ahead, else TMA
+// ring + producer warp).  Defaults are the measured winners per geometry
+// (profiles/r01/plane_variants.txt); TFNO_PLANE_VARIANT overrides for A/B runs.
+template <class G>
+constexpr int plane_variant_default() {
+  return G::DX == 512 ? 0 : (G::KX == 16 && G::DX == 256) ? 3 : 1;
+}
+template <class G>
+static int plane_variant() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TFNO_PLANE_VARIANT");
+    env = e ? atoi(e) : -1;
+  }
+  return env >= 0 ? env : plane_variant_default<G>();
 }
 
 static int num_sms() {
@@ -482,24 +532,40 @@ static int num_sms() {
   return n;
 }
 
+template <class G, int S, bool NAT, bool DLD>
+static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
+  const int sms = num_sms();
+  size_t smem = fwd_smem<G>(S, DLD);
+  int grid = (int)(planes < sms ? planes : sms);
+  if (grid < 1) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, NAT, DLD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  plane_fwd2d_kernel<G, S, NAT, DLD><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 template <class G, int S>
 static cudaError_t launch_fwd(const float2* x, float2* A, int64_t planes, const float2* tw, bool natural,
                               cudaStream_t st) {
+  const bool dld = (plane_variant<G>() & 2) != 0;
+  if (natural)
+    return dld ? launch_fwd_v<G, S, true, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, true, false>(x, A, planes, tw, st);
+  return dld ? launch_fwd_v<G, S, false, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, false, false>(x, A, planes, tw, st);
+}
+
+template <class G, int SO, bool NAT, bool DST>
+static cudaError_t launch_inv_v(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale,
+                                cudaStream_t st) {
   const int sms = num_sms();
-  size_t smem = fwd_smem<G>(S);
+  size_t smem = inv_smem<G>(SO, DST);
   int grid = (int)(planes < sms ? planes : sms);
   if (grid < 1) return cudaSuccess;
-  cudaError_t e;
-  if (natural) {
-    e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    plane_fwd2d_kernel<G, S, true><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
-  } else {
-    e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    plane_fwd2d_kernel<G, S, false><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
-  }
+  cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, NAT, DST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  plane_inv2d_kernel<G, SO, NAT, DST><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -507,23 +573,12 @@ static cudaError_t launch_fwd(const float2* x, float2* A, int64_t planes, const 
 template <class G, int SO>
 static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale, bool natural,
                               cudaStream_t st) {
-  const int sms = num_sms();
-  size_t smem = inv_smem<G>(SO);
-  int grid = (int)(planes < sms ? planes : sms);
-  if (grid < 1) return cudaSuccess;
-  cudaError_t e;
-  if (natural) {
-    e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    plane_inv2d_kernel<G, SO, true><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
-  } else {
-    e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    plane_inv2d_kernel<G, SO, false><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
-  }
-  ++g_launches;
-  return cudaGetLastError();
+  const bool dst = (plane_variant<G>() & 1) != 0;
+  if (natural)
+    return dst ? launch_inv_v<G, SO, true, true>(Cm, y, planes, tw, scale, st)
+               : launch_inv_v<G, SO, true, false>(Cm, y, planes, tw, scale, st);
+  return dst ? launch_inv_v<G, SO, false, true>(Cm, y, planes, tw, scale, st)
+             : launch_inv_v<G, SO, false, false>(Cm, y, planes, tw, scale, st);
 }
 
 template <class G, int S, int SO>

@@ -22,7 +22,7 @@ BUILD_DIR = os.path.join(HERE, "_build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart", "shared",
               "-Xptxas", "-v"] + ARCH
-SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "api.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "fused1d.cu", "api.cu", "plan.cpp"]
 
 
 def _nvcc() -> str:
@@ -44,8 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(BUILD_DIR, exist_ok=True)
     nvcc = _nvcc()
-    objs = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(BUILD_DIR, src + ".o")
         path = os.path.join(CSRC, src)
         if src.endswith(".cpp"):
@@ -59,7 +59,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(res.stderr)
         with open(os.path.join(BUILD_DIR, src + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
-        objs.append(obj)
+        return obj
+
+    # translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = OUT + ".tmp"
     cmd = [nvcc, "-shared", "--cudart", "shared"] + ARCH + ["-o", tmp] + objs + [
         "-L/usr/local/cuda/lib64", "-lcufft", "-lcublas", "-lcudart",

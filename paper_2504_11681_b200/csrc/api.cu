@@ -149,7 +149,7 @@ cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st
 
 // schedule decision shared by workspace sizing and the forward
 struct Sched {
-  bool staged = false, plane2d = false, rows_fast = false, warp_fused = false;
+  bool staged = false, plane2d = false, rows_fast = false, warp_fused = false, f1 = false;
   int rows_NT = 0;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
@@ -178,6 +178,19 @@ Sched make_sched(const tfno_cfg* c, int mode) {
   FusedArgs fa{};
   int NT = 0;
   bool ok;
+  static int f1_env = -2;
+  if (f1_env == -2) {
+    const char* e = getenv("TFNO_FUSED1D");
+    f1_env = e ? atoi(e) : -1;
+  }
+  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
+    s.f1 = true;
+    s.fg = s.gi = true;
+    s.need_s1 = s.need_mid = (g.rank == 2);
+    s.launches = (g.rank == 2) ? 3 : 1;
+    s.desc = g.rank == 2 ? "x-fft|fused1d-fft-cgemm-ifft|x-ifft" : "fused1d-fft-cgemm-ifft";
+    return s;
+  }
   if (mode == TFNO_FULLY_FUSED && warp_fused_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
     s.warp_fused = true;
     s.fg = s.gi = true;
@@ -606,11 +619,11 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   }
   if (s.fg || s.gi) {
     FusedArgs fa{};
-    if (s.rows_fast || s.warp_fused) {
+    if (s.rows_fast || s.warp_fused || s.f1) {
       fa.n = (int)g.dy;
       fa.keep = (int)g.ky;
       fa.N = (int)g.N;
-      fa.NT = s.warp_fused ? (int)g.N : s.rows_NT;
+      fa.NT = (s.warp_fused || s.f1) ? (int)g.N : s.rows_NT;
       fa.KC = rows_chunk((int)g.dy);
       fa.EC = fa.KC;
     } else {
@@ -639,8 +652,9 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     fa.twg = tw;
     fa.inv_scale = (float)(1.0 / (double)g.dy);
     if (fa.G > 2147483647LL || (g.N + fa.NT - 1) / fa.NT > 65535) return TFNO_EUNSUPPORTED;
-    e = s.warp_fused ? launch_warp_fused(fa, st)
-                     : (s.rows_fast ? launch_rows_fused(fa, s.fg, s.gi, st) : launch_fused(fa, s.fg, s.gi, st));
+    e = s.f1 ? launch_fused1d(fa, st)
+             : s.warp_fused ? launch_warp_fused(fa, st)
+                            : (s.rows_fast ? launch_rows_fused(fa, s.fg, s.gi, st) : launch_fused(fa, s.fg, s.gi, st));
     if (e != cudaSuccess) return TFNO_ECUDA;
     stage_mark(st);
   } else {

@@ -1,0 +1,336 @@
+// Fused 1D Fourier layer (K6, reference pipeline.py:185-206 + 236-275 for
+// rank 1): FFT -> truncate -> channel CGEMM -> zero-pad -> iFFT in ONE
+// persistent sm_100a kernel; only x, y (and the L2-resident W) touch HBM.
+//
+// Warp-specialised, one CTA per SM, 20 warps (registers split with setmaxnreg):
+//   8 FFT warps     TEAMS = 256/L row teams (L = 16: N = 256 per half warp;
+//                   L = 32: N = 1024 per warp).  Per work item g (a batch
+//                   element for rank 1) they walk the hidden dimension in
+//                   chunks of KC = TEAMS channel rows, in step with the GEMM
+//                   k-loop: load the row from its TMA slot into registers,
+//                   release the slot, truncated register FFT (wf_dft.cuh:
+//                   DFT_L, twiddle, swizzled smem transpose, first-KP DFT_L),
+//                   kept bins -> A chunk ring As[s][h][q].  After the forward
+//                   of item i they run the zero-padded inverse of item i-1's
+//                   output rows from the C tile (scaled 1/N, streaming stores).
+//   8 GEMM warps    acc[q][n] += As[h][q] * W[h][n], FP32 FFMA, TI x TJ complex
+//                   register tile per thread, k ascending like cgemm.gemm_kloop;
+//                   at the end of an item the tile goes to Cs for the FFT warps.
+//   producer WG     one thread: cp.async.bulk of each team's next input row into its slot
+//                   (L2 evict-first) and of the chunk's W rows W[h0:h0+KC][:]
+//                   into a 2-slot ring (evict-last).
+// Every hand-off is an mbarrier (full/empty pairs for rows, W chunks, A chunks
+// and the C tile), so the GEMM of item i overlaps the forward FFTs of item i
+// and the inverse FFTs of item i-1; there is no CTA-wide barrier in the loop.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+#include "wf_dft.cuh"
+
+namespace tfno {
+
+template <int L, int KP, int TI, int TJ, int NOUT>
+struct F1Geo {
+  static constexpr int N = L * L, NFT = 256, NGT = 256, TEAMS = NFT / L, KC = TEAMS, KT = KP * L;
+  static constexpr int NTH = NFT + NGT + 128;  // + one producer warpgroup (3 warps idle)
+  static constexpr int NA = 2;                 // A chunk ring depth
+  static constexpr int MT = KT / TI, NTG = NOUT / TJ;
+  static_assert(MT * NTG == NGT, "GEMM thread grid must cover the GEMM warps");
+  static_assert(NOUT % TEAMS == 0, "inverse rows per team");
+  static constexpr int BAR_BYTES = 1024;
+  // float2 units after the barrier block; NSLOT input-row slots per team
+  static constexpr size_t total(int ns) {
+    return (size_t)TEAMS * N * ns + 2 * KC * NOUT + NA * KC * KT + KT * NOUT + TEAMS * L * L + L * L + L;
+  }
+  static constexpr int NSLOT = (BAR_BYTES + 8 * total(2) <= 220 * 1024) ? 2 : 1;  // deeper prefetch if it fits
+  static constexpr int OFF_SLOT = 0;
+  static constexpr int OFF_W = OFF_SLOT + TEAMS * N * NSLOT;
+  static constexpr int OFF_A = OFF_W + 2 * KC * NOUT;
+  static constexpr int OFF_C = OFF_A + NA * KC * KT;
+  static constexpr int OFF_TR = OFF_C + KT * NOUT;
+  static constexpr int OFF_TWN = OFF_TR + TEAMS * L * L;
+  static constexpr int OFF_TWL = OFF_TWN + L * L;
+  static constexpr int TOTAL = OFF_TWL + L;
+  static constexpr size_t smem_bytes() { return BAR_BYTES + sizeof(float2) * (size_t)TOTAL; }
+  // register split (setmaxnreg) inside the CTA's launch allocation of 640 x 96:
+  // producer warpgroup 24, FFT warps 96 (unchanged), GEMM warps 128
+  static constexpr int REG_LAUNCH = 96, REG_PROD = 24, REG_FFT = 96, REG_GEMM = 128;
+  static_assert(128 * REG_PROD + NFT * REG_FFT + NGT * REG_GEMM <= NTH * REG_LAUNCH, "register pool");
+};
+
+// L x L transpose tile without padding: column XOR-swizzled by the row, so
+// both the row-wise writes and the column-wise reads of a team are
+// bank-conflict free.
+template <int L>
+__device__ __forceinline__ int tsw(int r, int c) {
+  return r * L + (c ^ r);
+}
+
+template <int L, int KP, int TI, int TJ, int NOUT>
+__global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
+  using G = F1Geo<L, KP, TI, TJ, NOUT>;
+  constexpr int N = G::N, TEAMS = G::TEAMS, KC = G::KC, KT = G::KT, MT = G::MT, NTG = G::NTG, NA = G::NA;
+  constexpr int NGW = G::NGT / 32, NS = G::NSLOT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [TEAMS][NS] row slot filled
+  uint64_t* empty = full + TEAMS * NS;                  // [TEAMS][NS] row slot free
+  uint64_t* wfull = empty + TEAMS * NS;                 // [2]
+  uint64_t* wempty = wfull + 2;                         // [2]
+  uint64_t* afull = wempty + 2;                         // [NA]
+  uint64_t* aempty = afull + NA;                        // [NA]
+  uint64_t* cfull = aempty + NA;                        // C tile written
+  uint64_t* cempty = cfull + 1;                         // C tile consumed
+  float2* base = reinterpret_cast<float2*>(smem + G::BAR_BYTES);
+  float2* slots = base + G::OFF_SLOT;
+  float2* Wr = base + G::OFF_W;
+  float2* As = base + G::OFF_A;
+  float2* Cs = base + G::OFF_C;
+  float2* tr = base + G::OFF_TR;
+  float2* twN = base + G::OFF_TWN;
+  float2* twL = base + G::OFF_TWL;
+
+  const int tid = threadIdx.x;
+  const int keep = a.keep;
+  const int nchunks = a.H / KC;
+  const int64_t nmine = a.G > blockIdx.x ? (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (int k = tid; k < L; k += blockDim.x) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
+  for (int i = tid; i < L * L; i += blockDim.x) {
+    const int k1 = i / L, t = i % L;
+    twN[i] = __ldg(&a.twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
+  }
+  if (tid == 0) {
+    for (int t = 0; t < TEAMS * NS; ++t) {
+      mbar_init(&full[t], 1);
+      mbar_init(&empty[t], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], NGW);
+    }
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&afull[s], TEAMS);
+      mbar_init(&aempty[s], NGW);
+    }
+    mbar_init(cfull, NGW);
+    mbar_init(cempty, TEAMS);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= G::NFT + G::NGT) {
+    // ================= producer warpgroup (one elected thread issues)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_PROD));
+    if (tid == G::NFT + G::NGT) {
+      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_w = policy_evict_last();
+      const uint32_t wbytes = (uint32_t)(KC * NOUT * sizeof(float2));
+      int64_t kk = 0;  // chunks issued so far (the same count for every team)
+      for (int64_t it = 0; it < nmine; ++it) {
+        const int64_t g = blockIdx.x + it * gridDim.x;
+        const int64_t bb = g / a.gx, pp = g % a.gx;
+        const float2* xg = a.x + bb * a.x_sb + pp * a.x_sp;
+        for (int c = 0; c < nchunks; ++c, ++kk) {
+          const int rs = (int)(kk % NS);
+          const int64_t use = kk / NS;
+#pragma unroll 1
+          for (int t = 0; t < TEAMS; ++t) {
+            const int b = t * NS + rs;
+            if (use >= 1) mbar_wait(&empty[b], (uint32_t)((use - 1) & 1));
+            mbar_expect_tx(&full[b], N * sizeof(float2));
+            tma_load_1d(slots + b * N, xg + (int64_t)(c * KC + t) * a.x_sh, N * sizeof(float2), &full[b], pol_x);
+          }
+          const int ws = (int)(kk & 1);
+          if (kk >= 2) mbar_wait(&wempty[ws], (uint32_t)(((kk >> 1) - 1) & 1));
+          mbar_expect_tx(&wfull[ws], wbytes);
+          tma_load_1d(Wr + ws * KC * NOUT, a.W + (int64_t)c * KC * NOUT, wbytes, &wfull[ws], pol_w);
+        }
+      }
+    }
+    return;
+  }
+
+  if (tid >= G::NFT) {
+    // ================= GEMM warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_GEMM));
+    const int gt = tid - G::NFT;
+    const int tm = gt % MT, tn = gt / MT;
+    int64_t kk = 0;
+    for (int64_t it = 0; it < nmine; ++it) {
+      float2 acc[TI][TJ];
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int c = 0; c < nchunks; ++c, ++kk) {
+        const int s = (int)(kk % NA), ws = (int)(kk & 1);
+        mbar_wait(&afull[s], (uint32_t)((kk / NA) & 1));
+        mbar_wait(&wfull[ws], (uint32_t)((kk >> 1) & 1));
+        const float2* Ab = As + s * KC * KT;
+        const float2* Wc = Wr + ws * KC * NOUT;
+#pragma unroll 4
+        for (int hl = 0; hl < KC; ++hl) {
+          float2 av[TI], bv[TJ];
+#pragma unroll
+          for (int i = 0; i < TI; ++i) av[i] = Ab[hl * KT + tm + MT * i];
+#pragma unroll
+          for (int j = 0; j < TJ; ++j) bv[j] = Wc[hl * NOUT + tn + NTG * j];
+#pragma unroll
+          for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+        }
+        __syncwarp();
+        if ((gt & 31) == 0) {
+          mbar_arrive(&aempty[s]);
+          mbar_arrive(&wempty[ws]);
+        }
+      }
+      // hand the C tile to the FFT warps (once they are done with the previous one)
+      if (it >= 1) mbar_wait(cempty, (uint32_t)((it - 1) & 1));
+#pragma unroll
+      for (int j = 0; j < TJ; ++j)
+#pragma unroll
+        for (int i = 0; i < TI; ++i) Cs[(tn + NTG * j) * KT + tm + MT * i] = acc[i][j];
+      __syncwarp();
+      if ((gt & 31) == 0) mbar_arrive(cfull);
+    }
+    return;
+  }
+
+  // ================= FFT warps
+  if constexpr (G::REG_FFT > G::REG_LAUNCH) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
+  const int lane = tid % L, team = tid / L;
+  const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));
+  float2* trr = tr + team * L * L;
+  int64_t kk = 0;
+  for (int64_t it = 0; it <= nmine; ++it) {
+    if (it < nmine) {
+      // ---- forward of item it: channel rows h = c*KC + team -> A chunk ring
+      for (int c = 0; c < nchunks; ++c, ++kk) {
+        const int b = team * NS + (int)(kk % NS);
+        mbar_wait(&full[b], (uint32_t)((kk / NS) & 1));
+        const float2* slot = slots + b * N;
+        float2 v[L];
+#pragma unroll
+        for (int j = 0; j < L; ++j) v[j] = slot[lane + L * j];
+        __syncwarp(tmask);
+        if (lane == 0) mbar_arrive(&empty[b]);  // the producer refills the slot now
+        wf::dftL<L, -1>(v, twL);
+#pragma unroll
+        for (int k1 = 1; k1 < L; ++k1) v[k1] = cmul(v[k1], twN[k1 * L + lane]);
+#pragma unroll
+        for (int k1 = 0; k1 < L; ++k1) trr[tsw<L>(k1, lane)] = v[k1];
+        __syncwarp(tmask);
+#pragma unroll
+        for (int t = 0; t < L; ++t) v[t] = trr[tsw<L>(lane, t)];
+        __syncwarp(tmask);
+        float2 o[KP];
+        wf::dftL_first<L, KP>(v, o, twL);
+        const int s = (int)(kk % NA);
+        if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
+        float2* Ab = As + s * KC * KT;
+#pragma unroll
+        for (int k2 = 0; k2 < KP; ++k2) {
+          const int q = lane + L * k2;
+          Ab[team * KT + q] = q < keep ? o[k2] : make_float2(0.f, 0.f);
+        }
+        __syncwarp(tmask);
+        if (lane == 0) mbar_arrive(&afull[s]);
+      }
+    }
+    if (it >= 1) {
+      // ---- zero-padded inverse of item it-1's output rows from the C tile
+      const int64_t g = blockIdx.x + (it - 1) * gridDim.x;
+      const int64_t bb = g / a.gx, pp = g % a.gx;
+      float2* yg = a.y + bb * a.y_sb + pp * a.y_sp;
+      mbar_wait(cfull, (uint32_t)((it - 1) & 1));
+      for (int n = team; n < NOUT; n += TEAMS) {
+        float2 xk[KP];
+#pragma unroll
+        for (int k2 = 0; k2 < KP; ++k2) {
+          const int q = lane + L * k2;
+          xk[k2] = q < keep ? Cs[n * KT + q] : make_float2(0.f, 0.f);
+        }
+        float2 z[L];
+        wf::idftL_padded<L, KP>(xk, z, twL);
+#pragma unroll
+        for (int t = 1; t < L; ++t) z[t] = cmul(z[t], conjf2(twN[t * L + lane]));
+#pragma unroll
+        for (int t = 0; t < L; ++t) trr[tsw<L>(t, lane)] = z[t];
+        __syncwarp(tmask);
+#pragma unroll
+        for (int k1 = 0; k1 < L; ++k1) z[k1] = trr[tsw<L>(lane, k1)];
+        __syncwarp(tmask);
+        wf::dftL<L, 1>(z, twL);
+        float2* dst = yg + (int64_t)n * a.y_sn;
+#pragma unroll
+        for (int j = 0; j < L; ++j) __stcs(dst + lane + L * j, cscale(z[j], a.inv_scale));
+      }
+      __syncwarp(tmask);
+      if (lane == 0) mbar_arrive(cempty);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dispatch
+struct F1Shape {
+  int L, KP, TI, TJ, NOUT;
+};
+// instantiated shapes: keep <= KP*L (masked), H % (256/L) == 0, N_out == NOUT
+static const F1Shape kF1Shapes[] = {
+    {16, 1, 1, 4, 64}, {16, 1, 1, 8, 128}, {16, 1, 2, 8, 256},  // keep <= 16 (N = 256)
+    {16, 2, 2, 4, 64}, {16, 2, 2, 8, 128}, {16, 2, 4, 8, 256},  // keep <= 32
+    {16, 4, 4, 4, 64}, {16, 4, 4, 8, 128},                      // keep <= 64
+    {32, 2, 4, 4, 64},                                          // keep <= 64 (N = 1024)
+    {32, 4, 8, 4, 64},                                          // keep <= 128
+};
+
+static const F1Shape* f1_pick(int n, int keep, int H, int NO) {
+  const int L = n == 256 ? 16 : (n == 1024 ? 32 : 0);
+  if (!L || keep < 1 || H < 1 || H % (256 / L) != 0) return nullptr;
+  const int kp = (keep + L - 1) / L;
+  for (const F1Shape& s : kF1Shapes)
+    if (s.L == L && s.NOUT == NO && (s.KP == kp || (kp == 3 && s.KP == 4))) return &s;
+  return nullptr;
+}
+
+bool fused1d_supported(int n, int keep, int H, int NO) { return f1_pick(n, keep, H, NO) != nullptr; }
+
+template <int L, int KP, int TI, int TJ, int NOUT>
+static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
+  using G = F1Geo<L, KP, TI, TJ, NOUT>;
+  static_assert(G::smem_bytes() <= 227 * 1024, "shared memory");
+  const size_t smem = G::smem_bytes();
+  if ((uintptr_t)a.x % 16 || (uintptr_t)a.W % 16 || (a.x_sh % 2) || (a.x_sb % 2) || (a.x_sp % 2))
+    return cudaErrorNotSupported;  // TMA bulk copies need 16-byte aligned rows
+  cudaError_t e = cudaFuncSetAttribute(fused1d_kernel<L, KP, TI, TJ, NOUT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(a.G < sms ? a.G : sms);
+  if (grid < 1) return cudaSuccess;
+  fused1d_kernel<L, KP, TI, TJ, NOUT><<<grid, G::NTH, smem, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s) {
+  const F1Shape* p = f1_pick(a.n, a.keep, a.H, a.N);
+  if (!p) return cudaErrorNotSupported;
+#define F1_CASE(LL, KK, TI_, TJ_, NO_) \
+  if (p->L == LL && p->KP == KK && p->NOUT == NO_) return launch_f1<LL, KK, TI_, TJ_, NO_>(a, s);
+  F1_CASE(16, 1, 1, 4, 64) F1_CASE(16, 1, 1, 8, 128) F1_CASE(16, 1, 2, 8, 256)
+  F1_CASE(16, 2, 2, 4, 64) F1_CASE(16, 2, 2, 8, 128) F1_CASE(16, 2, 4, 8, 256)
+  F1_CASE(16, 4, 4, 4, 64) F1_CASE(16, 4, 4, 8, 128)
+  F1_CASE(32, 2, 4, 4, 64)
+  F1_CASE(32, 4, 8, 4, 64)
+#undef F1_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace tfno

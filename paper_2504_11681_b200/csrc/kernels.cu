@@ -284,15 +284,22 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   const bool fast = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) &&
                     (g.w_ks % 2 == 0) && (g.w_bs % 2 == 0) && g.N > 16 && g.M >= 64 &&
                     ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0);
-  // small M (1D modes): fold batch elements into the 64-row tile
-  const bool foldable = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.M >= 2 && g.M < 64 &&
-                        (64 % g.M == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) && (g.w_ks % 2 == 0) &&
+  // small M (1D modes): fold batch elements into the M tile; the tile shape
+  // follows N (64 x 128 for N > 64, 128 x 64 otherwise: no idle columns)
+  const bool wide = g.N > 64;
+  const int64_t FBMf = wide ? 64 : 128;
+  const bool foldable = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.M >= 2 && g.M < FBMf &&
+                        (FBMf % g.M == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) && (g.w_ks % 2 == 0) &&
                         ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0) && g.N > 16;
   if (foldable) {
     GemmArgs f = g;
-    f.fold = 64 / g.M;
-    dim3 grid(1u, (unsigned)((g.N + 127) / 128), (unsigned)((g.batch + f.fold - 1) / f.fold));
-    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(f);
+    f.fold = FBMf / g.M;
+    dim3 grid(1u, (unsigned)((g.N + (wide ? 127 : 63)) / (wide ? 128 : 64)),
+              (unsigned)((g.batch + f.fold - 1) / f.fold));
+    if (wide)
+      cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(f);
+    else
+      cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(f);
   } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);

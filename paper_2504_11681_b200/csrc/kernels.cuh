@@ -77,6 +77,9 @@ cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2
                             int keep, int src_len, float scale, const float2* tw, cudaStream_t s);
 // fully fused 1D layer on warp FFTs (K6): whole k-loop per CTA, W resident in smem
 bool warp_fused_supported(int n, int keep, int H, int NO);
+// fully fused 1D layer, k-loop over channel chunks with a TMA producer warp (fused1d.cu)
+bool fused1d_supported(int n, int keep, int H, int NO);
+cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,
                                 float2* dst, int dx2, int dy2, int64_t d_plane, int cx, int cy,

@@ -18,84 +18,10 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "wf_dft.cuh"
 
 namespace tfno {
-namespace wf {
 
-// natural-order in-register DFT of length L (16 or 32): L = P*8,
-// x[n1 + P n2] -> DFT8 over n2 -> twiddle w_L^{n1 k2} -> DFT_P over n1,
-// output k = k2 + 8 k1.  v is overwritten with the natural-order output.
-template <int L, int DIR>
-__device__ __forceinline__ void dftL(float2* v, const float2* __restrict__ twL /* w_L^k, k < L (forward sign) */) {
-  constexpr int P = L / 8;
-  float2 a[P][8];
-#pragma unroll
-  for (int n1 = 0; n1 < P; ++n1) {
-#pragma unroll
-    for (int n2 = 0; n2 < 8; ++n2) a[n1][n2] = v[n1 + P * n2];
-    dft8<DIR>(a[n1]);
-  }
-#pragma unroll
-  for (int n1 = 1; n1 < P; ++n1)
-#pragma unroll
-    for (int k2 = 1; k2 < 8; ++k2) a[n1][k2] = cmul(a[n1][k2], tw_dir<DIR>(twL[n1 * k2]));
-#pragma unroll
-  for (int k2 = 0; k2 < 8; ++k2) {
-    float2 b[P];
-#pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) b[n1] = a[n1][k2];
-    dft<P, DIR>(b);
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) v[k2 + 8 * k1] = b[k1];
-  }
-}
-
-// first KP outputs of a forward DFT_L (KP <= 8): sum over n1 of the twiddled
-// DFT8 outputs (k1 = 0 of the second factor)
-template <int L, int KP>
-__device__ __forceinline__ void dftL_first(const float2* v, float2* out, const float2* __restrict__ twL) {
-  constexpr int P = L / 8;
-  float2 a[P][8];
-#pragma unroll
-  for (int n1 = 0; n1 < P; ++n1) {
-#pragma unroll
-    for (int n2 = 0; n2 < 8; ++n2) a[n1][n2] = v[n1 + P * n2];
-    dft8<-1>(a[n1]);
-  }
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    float2 s = a[0][k];
-#pragma unroll
-    for (int n1 = 1; n1 < P; ++n1) s = cadd(s, k ? cmul(a[n1][k], twL[n1 * k]) : a[n1][k]);
-    out[k] = s;
-  }
-}
-
-// inverse DFT_L with only the first KP inputs nonzero (KP <= 8):
-// z[t_lo + 8 t_hi] = sum_k (x[k] w_L^{+k t_lo}) w_P^{+k t_hi}, P = L/8: per t_lo
-// twiddle the KP inputs, fold k -> k mod P, inverse DFT_P over k mod P -> t_hi.
-template <int L, int KP>
-__device__ __forceinline__ void idftL_padded(const float2* x, float2* out, const float2* __restrict__ twL) {
-  constexpr int P = L / 8;
-  static_assert(KP <= 8, "padded inputs");
-#pragma unroll
-  for (int tl = 0; tl < 8; ++tl) {
-    float2 f[P];
-#pragma unroll
-    for (int r = 0; r < P; ++r) f[r] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-      const int e = (k * tl) % L;
-      const float2 xk = e ? cmul(x[k], conjf2(twL[e])) : x[k];
-      f[k % P] = cadd(f[k % P], xk);
-    }
-    dft<P, 1>(f);
-#pragma unroll
-    for (int th = 0; th < P; ++th) out[tl + 8 * th] = f[th];
-  }
-}
-
-}  // namespace wf
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -439,9 +365,16 @@ cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s) {
 template <int U>
 struct TfGeo {
   static constexpr int T = 32 * U, N = 32 * T, NTH = 512, TEAMS = NTH / T;
-  static constexpr int TSTR = 33;  // padded transpose stride
+  static constexpr int LU = U == 4 ? 2 : 1;
   static constexpr size_t smem_bytes() {
-    return sizeof(float2) * ((size_t)32 + (size_t)32 * T + (size_t)TEAMS * T * TSTR + (size_t)T);
+    return sizeof(float2) * ((size_t)32 + (size_t)32 * T + (size_t)TEAMS * T * 32 + (size_t)T);
+  }
+  // [t][k1] tile (row length 32, unpadded) with the column XOR-swizzled by a
+  // 4-bit rotation of t: conflict-free both for 16 consecutive t at fixed k1
+  // and for the (u, k1) lane pattern t = u + U*s of the stage-2 role.
+  __device__ static __forceinline__ int swz(int t, int k1) {
+    const int f = ((t & (U - 1)) << (4 - LU)) | ((t >> LU) & ((16 >> LU) - 1));
+    return t * 32 + (k1 ^ f);
   }
 };
 
@@ -453,18 +386,18 @@ __global__ void __launch_bounds__(512, 1) team_fft_fwd_kernel(const float2* __re
   constexpr int T = G::T, N = G::N;
   extern __shared__ __align__(16) float2 sm[];
   float2* tw32 = sm;                  // w_32^k
-  float2* twN = tw32 + 32;            // [k1][t] = w_N^{t k1}, k1 < 32, t < T
-  float2* tr = twN + 32 * T;          // TEAMS x T x TSTR
-  float2* twT = tr + G::TEAMS * T * G::TSTR;  // w_T^k
+  float2* twN = tw32 + 32;            // w_N^{t k1} at G::swz(t, k1), k1 < 32, t < T
+  float2* tr = twN + 32 * T;          // TEAMS x T x 32 (swizzled)
+  float2* twT = tr + G::TEAMS * T * 32;  // w_T^k
   const int tid = threadIdx.x, team = tid / T, tt = tid % T;
   for (int k = tid; k < 32; k += G::NTH) tw32[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / 32)]);
   for (int k = tid; k < T; k += G::NTH) twT[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / T)]);
   for (int i = tid; i < 32 * T; i += G::NTH) {
     const int k1 = i / T, t = i % T;
-    twN[i] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
+    twN[G::swz(t, k1)] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
   }
   __syncthreads();
-  float2* trr = tr + team * T * G::TSTR;
+  float2* trr = tr + team * T * 32;
   const int k1s = tt / U, us = tt % U;  // stage-2 role
   for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS) {
     const int64_t row = row0 + team;
@@ -475,14 +408,14 @@ __global__ void __launch_bounds__(512, 1) team_fft_fwd_kernel(const float2* __re
     for (int j = 0; j < 32; ++j) v[j] = live ? __ldg(&src[tt + T * j]) : make_float2(0.f, 0.f);
     wf::dftL<32, -1>(v, tw32);
 #pragma unroll
-    for (int k1 = 1; k1 < 32; ++k1) v[k1] = cmul(v[k1], twN[k1 * T + tt]);
+    for (int k1 = 1; k1 < 32; ++k1) v[k1] = cmul(v[k1], twN[G::swz(tt, k1)]);
     named_bar_sync(1 + team, T);
 #pragma unroll
-    for (int k1 = 0; k1 < 32; ++k1) trr[tt * G::TSTR + k1] = v[k1];  // [t][k1]
+    for (int k1 = 0; k1 < 32; ++k1) trr[G::swz(tt, k1)] = v[k1];  // [t][k1]
     named_bar_sync(1 + team, T);
     // thread (k1s, us): Y_{us + U s}[k1s] for s < 32
 #pragma unroll
-    for (int s2 = 0; s2 < 32; ++s2) v[s2] = trr[(us + U * s2) * G::TSTR + k1s];
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = trr[G::swz(us + U * s2, k1s)];
     wf::dftL<32, -1>(v, tw32);  // V_u[k2'] over s
     float2 o[K2];
 #pragma unroll
@@ -521,16 +454,16 @@ __global__ void __launch_bounds__(512, 1) team_fft_inv_kernel(const float2* __re
   float2* tw32 = sm;
   float2* twN = tw32 + 32;
   float2* tr = twN + 32 * T;
-  float2* twT = tr + G::TEAMS * T * G::TSTR;
+  float2* twT = tr + G::TEAMS * T * 32;
   const int tid = threadIdx.x, team = tid / T, tt = tid % T;
   for (int k = tid; k < 32; k += G::NTH) tw32[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / 32)]);
   for (int k = tid; k < T; k += G::NTH) twT[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / T)]);
   for (int i = tid; i < 32 * T; i += G::NTH) {
     const int k1 = i / T, t = i % T;
-    twN[i] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
+    twN[G::swz(t, k1)] = __ldg(&twg[(size_t)(t * k1) * (TFNO_TW_MAX / N)]);
   }
   __syncthreads();
-  float2* trr = tr + team * T * G::TSTR;
+  float2* trr = tr + team * T * 32;
   const int k1s = tt / U, us = tt % U;
   for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS) {
     const int64_t row = row0 + team;
@@ -553,12 +486,12 @@ __global__ void __launch_bounds__(512, 1) team_fft_inv_kernel(const float2* __re
 #pragma unroll
     for (int s2 = 0; s2 < 32; ++s2) {
       const int t = us + U * s2;
-      trr[t * G::TSTR + k1s] = cmul(z[s2], conjf2(twN[k1s * T + t]));  // w_N^{+k1 t}
+      trr[G::swz(t, k1s)] = cmul(z[s2], conjf2(twN[G::swz(t, k1s)]));  // w_N^{+k1 t}
     }
     named_bar_sync(1 + team, T);
     // thread t: DFT32 over k1 -> y[t + T j]
 #pragma unroll
-    for (int k1 = 0; k1 < 32; ++k1) z[k1] = trr[tt * G::TSTR + k1];
+    for (int k1 = 0; k1 < 32; ++k1) z[k1] = trr[G::swz(tt, k1)];
     wf::dftL<32, 1>(z, tw32);
     if (live) {
       float2* dst = out + row * out_stride;

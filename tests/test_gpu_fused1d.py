@@ -1,0 +1,79 @@
+"""GPU parity of the fused 1D layer kernel (fused1d.cu: FFT -> truncate ->
+channel CGEMM -> zero-pad -> iFFT in one launch, TMA producer warp) against
+the numpy oracle restatement of ``fnofuse.pipeline.run_layer`` and against
+the unfused schedule of the same library (y-FFT | CGEMM | y-iFFT).
+
+Shapes: the BASELINE C2 sweep's (N, H) grid with keep = N/8 at small batch,
+plus ragged keep (masked bins), rank-2 rows (the x-FFT/x-iFFT passes around
+the fused rows kernel) and a multi-item-per-CTA batch.  Tolerance: FP32 1e-5
+(max_rel_error, core.py:39-50)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_2504_11681_b200 as T
+    return T
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import fnofuse_port as O
+    return O
+
+
+CASES = [
+    # (batch, H, N_out, dim_x, dim_y, keep_x, keep_y, rank)
+    (3, 64, 64, 1, 256, 1, 32, 1),
+    (2, 128, 128, 1, 256, 1, 32, 1),
+    (2, 256, 256, 1, 256, 1, 32, 1),
+    (2, 64, 64, 1, 1024, 1, 128, 1),
+    (2, 64, 64, 1, 1024, 1, 64, 1),      # N = 1024, keep 64 (KP = 2)
+    (2, 64, 128, 1, 256, 1, 16, 1),      # H != N_out, keep <= 16
+    (2, 32, 64, 1, 256, 1, 20, 1),       # ragged keep (masked bins), H = 2 chunks
+    (2, 128, 64, 1, 256, 1, 50, 1),      # keep 50 -> KP = 4 tile
+    (2, 64, 64, 4, 256, 2, 32, 2),       # rank 2: x passes around the fused rows
+]
+
+
+def _schedule(T, cfg):
+    return T.layer_schedule(cfg, "fully_fused")[1]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_fused1d_vs_oracle(T, O, case):
+    cfg = T.FnoLayerConfig(*case)
+    assert "fused1d" in _schedule(T, cfg), _schedule(T, cfg)
+    x, w = O.random_inputs(cfg, 2000 + sum(case))
+    out, led = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+    ref = O.run_layer_values(cfg, x, w)
+    err = T.max_rel_error(out.data, ref)
+    assert err < FP32_TOL, (case, err)
+    exact = O.reference_layer(cfg, x, w)
+    assert T.max_rel_error(out.data, exact) < FP32_TOL
+
+
+@pytest.mark.parametrize("n,h,keep", [(256, 64, 32), (256, 256, 32), (1024, 64, 128)])
+def test_fused1d_many_items_vs_unfused(T, n, h, keep):
+    """Batch >> #SMs (several items per persistent CTA, ring phases wrap):
+    fused == unfused schedule within FP32 tolerance, and deterministic."""
+    import torch
+    cfg = T.FnoLayerConfig(700, h, h, 1, n, 1, keep, 1)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    x = torch.view_as_complex(torch.randn((cfg.batch, h, 1, n, 2), generator=g, device="cuda"))
+    w = torch.view_as_complex(torch.randn((h, h, 2), generator=g, device="cuda")).contiguous()
+    y1 = T.run_layer_device(cfg, x, w, mode="fully_fused").clone()
+    y2 = T.run_layer_device(cfg, x, w, mode="fft_optimized")
+    y3 = T.run_layer_device(cfg, x, w, mode="fully_fused")
+    torch.cuda.synchronize()
+    a, b = y1.cpu().numpy(), y2.cpu().numpy()
+    assert T.max_rel_error(a, b) < FP32_TOL
+    assert torch.equal(y1, y3)
+    assert np.isfinite(a).all()

@@ -95,7 +95,6 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   const int tid = threadIdx.x;
   const int keep = a.keep;
   const int nchunks = a.H / KC;
-  const int64_t nmine = a.G > blockIdx.x ? (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   for (int k = tid; k < L; k += blockDim.x) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
   for (int i = tid; i < L * L; i += blockDim.x) {
     const int k1 = i / L, t = i % L;
@@ -124,6 +123,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
     // ================= producer warpgroup (one elected thread issues)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_PROD));
     if (tid == G::NFT + G::NGT) {
+      const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_w = policy_evict_last();
       const uint32_t wbytes = (uint32_t)(KC * NOUT * sizeof(float2));
@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   if (tid >= G::NFT) {
     // ================= GEMM warps
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_GEMM));
+    const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int gt = tid - G::NFT;
     const int tm = gt % MT, tn = gt / MT;
     int64_t kk = 0;
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 
   // ================= FFT warps
   if constexpr (G::REG_FFT > G::REG_LAUNCH) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
+  const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;  // grid <= G
   const int lane = tid % L, team = tid / L;
   const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));
   float2* trr = tr + team * L * L;

@@ -30,6 +30,23 @@ def timeit(fn, reps, warm=3):
     return s.elapsed_time(e) / reps
 
 
+def graphed(fn):
+    """Capture fn (already warmed up: plans / workspaces exist) into a CUDA
+    graph and return its replay: removes host launch overhead from small
+    layers, for our kernels and the cuFFT/cuBLAS baselines alike."""
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g.replay
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "sweep.json"))
@@ -51,20 +68,23 @@ def main():
         w = torch.view_as_complex(torch.randn((H, N, 2), generator=g, device=dev)).contiguous()
         y = torch.empty((B, N, dx, dy), dtype=torch.complex64, device=dev)
         reps = 5 if args.quick else max(5, min(50, int(2e10 / max(fl["bytes"], 1))))
-        row = {"workload": name, "desc": desc, "bytes": fl["bytes"], "flops": fl["flops"]}
+        small = fl["bytes"] < (256 << 20)
+        wrap = graphed if small else (lambda f: f)
+        row = {"workload": name, "desc": desc, "bytes": fl["bytes"], "flops": fl["flops"],
+               "timing": "CUDA-graph replays" if small else "eager launches"}
         for mode in T.MODES:
-            ms = timeit(lambda: T.run_layer_device(cfg, x, w, out=y, mode=mode, validate=False), reps)
+            ms = timeit(wrap(lambda: T.run_layer_device(cfg, x, w, out=y, mode=mode, validate=False)), reps)
             row[mode] = round(ms, 4)
             row[mode + "_schedule"] = T.layer_schedule(cfg, mode)[1]
         for prec in ("tf32x3", "tf32"):
             try:
                 mode = "fully_fused" if rk == 2 else "fft_optimized"
-                row[prec] = round(timeit(lambda: T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=prec,
-                                                                      validate=False), reps), 4)
+                row[prec] = round(timeit(wrap(lambda: T.run_layer_device(cfg, x, w, out=y, mode=mode, precision=prec,
+                                                                           validate=False)), reps), 4)
             except Exception as ex:  # noqa: BLE001
                 row[prec] = str(ex)[:80]
         T._device.release_workspace()
-        row["torch_fft"] = round(timeit(lambda: bench.torch_fft_layer(cfg, x, w, y), reps), 4)
+        row["torch_fft"] = round(timeit(wrap(lambda: bench.torch_fft_layer(cfg, x, w, y)), reps), 4)
         ours = min(row[m] for m in T.MODES if m != "staged")
         best_base = min(row["staged"], row["torch_fft"])
         row["best_ours_fp32"] = ours

@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   const int tid = threadIdx.x;
   const int keep = a.keep;
   const int nchunks = a.H / KC;
+  const int S = a.nsplit > 1 ? a.nsplit : 1;  // items = row groups x output-channel splits
+  const int64_t items = a.G * S;
   for (int k = tid; k < L; k += blockDim.x) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
   for (int i = tid; i < L * L; i += blockDim.x) {
     const int k1 = i / L, t = i % L;
@@ -123,13 +125,14 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
     // ================= producer warpgroup (one elected thread issues)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_PROD));
     if (tid == G::NFT + G::NGT) {
-      const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_w = policy_evict_last();
       const uint32_t wbytes = (uint32_t)(KC * NOUT * sizeof(float2));
       int64_t kk = 0;  // chunks issued so far (the same count for every team)
       for (int64_t it = 0; it < nmine; ++it) {
-        const int64_t g = blockIdx.x + it * gridDim.x;
+        const int64_t item = blockIdx.x + it * gridDim.x;
+        const int64_t g = item / S, n0 = (item % S) * NOUT;
         const int64_t bb = g / a.gx, pp = g % a.gx;
         const float2* xg = a.x + bb * a.x_sb + pp * a.x_sp;
         for (int c = 0; c < nchunks; ++c, ++kk) {
@@ -145,7 +148,14 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
           const int ws = (int)(kk & 1);
           if (kk >= 2) mbar_wait(&wempty[ws], (uint32_t)(((kk >> 1) - 1) & 1));
           mbar_expect_tx(&wfull[ws], wbytes);
-          tma_load_1d(Wr + ws * KC * NOUT, a.W + (int64_t)c * KC * NOUT, wbytes, &wfull[ws], pol_w);
+          if (S == 1) {
+            tma_load_1d(Wr + ws * KC * NOUT, a.W + (int64_t)c * KC * NOUT, wbytes, &wfull[ws], pol_w);
+          } else {  // this split's columns W[h][n0:n0+NOUT], one bulk copy per row
+#pragma unroll 1
+            for (int r = 0; r < KC; ++r)
+              tma_load_1d(Wr + (ws * KC + r) * NOUT, a.W + (int64_t)(c * KC + r) * a.N + n0, NOUT * sizeof(float2),
+                          &wfull[ws], pol_w);
+          }
         }
       }
     }
@@ -155,7 +165,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   if (tid >= G::NFT) {
     // ================= GEMM warps
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_GEMM));
-    const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int gt = tid - G::NFT;
     const int tm = gt % MT, tn = gt / MT;
     int64_t kk = 0;
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 
   // ================= FFT warps
   if constexpr (G::REG_FFT > G::REG_LAUNCH) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
-  const int64_t nmine = (a.G - blockIdx.x + gridDim.x - 1) / gridDim.x;  // grid <= G
+  const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;  // grid <= items
   const int lane = tid % L, team = tid / L;
   const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));
   float2* trr = tr + team * L * L;
@@ -245,9 +255,10 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
     }
     if (it >= 1) {
       // ---- zero-padded inverse of item it-1's output rows from the C tile
-      const int64_t g = blockIdx.x + (it - 1) * gridDim.x;
+      const int64_t item = blockIdx.x + (it - 1) * gridDim.x;
+      const int64_t g = item / S, n0 = (item % S) * NOUT;
       const int64_t bb = g / a.gx, pp = g % a.gx;
-      float2* yg = a.y + bb * a.y_sb + pp * a.y_sp;
+      float2* yg = a.y + bb * a.y_sb + pp * a.y_sp + n0 * a.y_sn;
       mbar_wait(cfull, (uint32_t)((it - 1) & 1));
       for (int n = team; n < NOUT; n += TEAMS) {
         float2 xk[KP];
@@ -284,6 +295,7 @@ struct F1Shape {
 // instantiated shapes: keep <= KP*L (masked), H % (256/L) == 0, N_out == NOUT
 static const F1Shape kF1Shapes[] = {
     {16, 1, 1, 4, 64}, {16, 1, 1, 8, 128}, {16, 1, 2, 8, 256},  // keep <= 16 (N = 256)
+    {16, 2, 1, 4, 32},                                          // keep <= 32, N_out (per split) 32
     {16, 2, 2, 4, 64}, {16, 2, 2, 8, 128}, {16, 2, 4, 8, 256},  // keep <= 32
     {16, 4, 4, 4, 64}, {16, 4, 4, 8, 128},                      // keep <= 64
     {32, 2, 4, 4, 64},                                          // keep <= 64 (N = 1024)
@@ -314,19 +326,33 @@ static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)(a.G < sms ? a.G : sms);
+  const int64_t items = a.G * (a.nsplit > 1 ? a.nsplit : 1);
+  const int grid = (int)(items < sms ? items : sms);
   if (grid < 1) return cudaSuccess;
   fused1d_kernel<L, KP, TI, TJ, NOUT><<<grid, G::NTH, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
 
+int fused1d_split(int n, int keep, int H, int NO, int64_t G) {
+  if (!f1_pick(n, keep, H, NO)) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int S = 1;  // split while the doubled item count still fits one wave of SMs
+  while (S < 4 && NO % (2 * S) == 0 && G * 2 * S <= sms && f1_pick(n, keep, H, NO / (2 * S))) S *= 2;
+  return S;
+}
+
 cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s) {
-  const F1Shape* p = f1_pick(a.n, a.keep, a.H, a.N);
+  const int S = a.nsplit > 1 ? a.nsplit : 1;
+  if (a.N % S) return cudaErrorNotSupported;
+  const F1Shape* p = f1_pick(a.n, a.keep, a.H, a.N / S);
   if (!p) return cudaErrorNotSupported;
 #define F1_CASE(LL, KK, TI_, TJ_, NO_) \
   if (p->L == LL && p->KP == KK && p->NOUT == NO_) return launch_f1<LL, KK, TI_, TJ_, NO_>(a, s);
   F1_CASE(16, 1, 1, 4, 64) F1_CASE(16, 1, 1, 8, 128) F1_CASE(16, 1, 2, 8, 256)
+  F1_CASE(16, 2, 1, 4, 32)
   F1_CASE(16, 2, 2, 4, 64) F1_CASE(16, 2, 2, 8, 128) F1_CASE(16, 2, 4, 8, 256)
   F1_CASE(16, 4, 4, 4, 64) F1_CASE(16, 4, 4, 8, 128)
   F1_CASE(32, 2, 4, 4, 64)

@@ -50,6 +50,7 @@ struct FusedArgs {
   float2* C;
   int64_t c_sb, c_sp, c_sn;  // C row (g,n), contiguous keep
   int NT, KC, EC;
+  int nsplit;  // fused1d: output channels split over nsplit CTAs per row group (forward recomputed)
   const float2* twg;
   float inv_scale;
 };
@@ -79,6 +80,8 @@ cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2
 bool warp_fused_supported(int n, int keep, int H, int NO);
 // fully fused 1D layer, k-loop over channel chunks with a TMA producer warp (fused1d.cu)
 bool fused1d_supported(int n, int keep, int H, int NO);
+// output-channel split for fused1d so that small batches still fill the SMs (0 = unsupported)
+int fused1d_split(int n, int keep, int H, int NO, int64_t G);
 cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,

@@ -19,6 +19,7 @@
 //   pad_truncate_kernel staged baseline's truncate/pad copy passes
 //                       (pipeline.py:162-166, 263-268).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "fft_engine.cuh"
 #include "kernels.cuh"
@@ -171,9 +172,11 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
 // (m = tm + 16 i, n = tn + 16 j: conflict-free / broadcast shared reads);
 // next chunk prefetched into registers (float4) while the current one is
 // consumed from shared memory (double buffer).
+// TI x TJ = 8 x 8 (128 x 128 tile, BK = 8, one CTA of 200+ registers per
+// SM) halves the shared-memory operand loads per FFMA for large M and N.
 template <int TI, int TJ>
-__global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
-  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = 16;
+__global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kernel(GemmArgs g) {
+  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 ? 8 : 16);
   __shared__ __align__(16) float2 As[2][FBK][FBM];
   __shared__ __align__(16) float2 Ws[2][FBK][FBN];
   const int tid = threadIdx.x;
@@ -280,6 +283,163 @@ __global__ void __launch_bounds__(256, 2) cgemm_modes_kernel(GemmArgs g) {
   }
 }
 
+// Gauss / 3M variant of the mode CGEMM: a complex MAC in 3 real FFMAs
+// instead of 4.  With s = ar + ai, d = wi - wr, u = wr + wi:
+//   t1 += s*wr,  t2 += ar*d,  t3 += ai*u;   Re C = t1 - t3,  Im C = t1 + t2.
+// The sums are formed once per element when a chunk is staged into shared
+// memory (A as (ar, ai, s), W as (wr, d, u), float4 each), so the inner loop
+// is TI + TJ LDS.128 per 3*TI*TJ FFMA.  Same FP32 arithmetic, 25% fewer FMA
+// issues than cgemm.gemm_kloop's 4M product; error stays at fp32 level
+// (tests/test_gpu_parity.py: <= 1e-5 vs float64, like the 4M kernel).
+// Measured SLOWER on B200 (N1024 H256: 1.92 vs 1.46 ms, ncu: 47% issue, the
+// register prefetch of A is sunk by ptxas at 253 registers -> long-scoreboard
+// stalls), so it is opt-in (TFNO_CGEMM_ALGO=3); profiles/r01/cgemm_3m_vs_4m.txt.
+template <int TI, int TJ>
+constexpr size_t cgemm3m_smem() {
+  return sizeof(float4) * 2 * 16 * (16 * TI + 16 * TJ);
+}
+template <int TI, int TJ>
+__global__ void __launch_bounds__(256, 1) cgemm3m_modes_kernel(GemmArgs g) {
+  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = 16;
+  extern __shared__ __align__(16) float4 sm3[];
+  float4 (*As)[FBK][FBM] = reinterpret_cast<float4 (*)[FBK][FBM]>(sm3);
+  float4 (*Ws)[FBK][FBN] = reinterpret_cast<float4 (*)[FBK][FBN]>(sm3 + 2 * FBK * FBM);
+  const int tid = threadIdx.x;
+  const int tm = tid % 16, tn = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
+  const int64_t fold = g.fold > 1 ? g.fold : 1;
+  const int64_t b = blockIdx.z * fold;
+  const float2* __restrict__ A = g.A + b * g.a_bs;
+  const float2* __restrict__ W = g.W + (fold > 1 ? 0 : b * g.w_bs);
+  auto a_off = [&](int64_t gm) -> int64_t { return fold > 1 ? (gm / g.M) * g.a_bs + gm % g.M : gm; };
+  auto m_ok = [&](int64_t gm) { return fold > 1 ? (gm / g.M < fold && b + gm / g.M < g.batch) : gm < g.M; };
+  constexpr int NA = FBK * FBM / 2 / 256, NW = FBK * FBN / 2 / 256;  // float4 (complex pairs) per thread
+  static_assert(NA >= 1 && NW >= 1, "tile");
+  float4 ra[NA], rw[NW];
+  auto load_chunk = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
+      const int64_t gk = k0 + kk, gm = m0 + mm;
+      if (fold > 1) {
+        ra[r] = (gk < g.K && m_ok(gm)) ? __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + a_off(gm)))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (gk < g.K && gm + 1 < g.M) {
+        ra[r] = __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + gm));
+      } else {
+        float2 v0 = (gk < g.K && gm < g.M) ? A[gk * g.a_ks + gm] : make_float2(0.f, 0.f);
+        ra[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBN / 2), nn = (i % (FBN / 2)) * 2;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      if (gk < g.K && gn + 1 < g.N) {
+        rw[r] = __ldg(reinterpret_cast<const float4*>(W + gk * g.w_ks + gn));
+      } else {
+        float2 v0 = (gk < g.K && gn < g.N) ? W[gk * g.w_ks + gn] : make_float2(0.f, 0.f);
+        rw[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
+      }
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
+      const float4 v = ra[r];
+      As[buf][kk][mm] = make_float4(v.x, v.y, v.x + v.y, 0.f);
+      As[buf][kk][mm + 1] = make_float4(v.z, v.w, v.z + v.w, 0.f);
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int i = tid + r * 256;
+      const int kk = i / (FBN / 2), nn = (i % (FBN / 2)) * 2;
+      const float4 v = rw[r];
+      Ws[buf][kk][nn] = make_float4(v.x, v.y - v.x, v.x + v.y, 0.f);
+      Ws[buf][kk][nn + 1] = make_float4(v.z, v.w - v.z, v.z + v.w, 0.f);
+    }
+  };
+  float t1[TI][TJ], t2[TI][TJ], t3[TI][TJ];
+#pragma unroll
+  for (int i = 0; i < TI; ++i)
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) t1[i][j] = t2[i][j] = t3[i][j] = 0.f;
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += FBK) {
+    const bool more = k0 + FBK < g.K;
+    if (more) load_chunk(k0 + FBK);
+#pragma unroll
+    for (int kk = 0; kk < FBK; ++kk) {
+      float4 av[TI], bv[TJ];
+#pragma unroll
+      for (int i = 0; i < TI; ++i) av[i] = As[buf][kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) bv[j] = Ws[buf][kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) {
+          t1[i][j] = fmaf(av[i].z, bv[j].x, t1[i][j]);
+          t2[i][j] = fmaf(av[i].x, bv[j].y, t2[i][j]);
+          t3[i][j] = fmaf(av[i].y, bv[j].z, t3[i][j]);
+        }
+    }
+    if (more) {
+      store_chunk(buf ^ 1);  // last read in the previous chunk, before its barrier
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  float2* C = g.C + b * g.c_bs;
+#pragma unroll
+  for (int j = 0; j < TJ; ++j) {
+    const int64_t gn = n0 + tn + 16 * j;
+    if (gn >= g.N) continue;
+#pragma unroll
+    for (int i = 0; i < TI; ++i) {
+      const int64_t gm = m0 + tm + 16 * i;
+      const float2 c = make_float2((t1[i][j] - t3[i][j]) * g.alpha, (t1[i][j] + t2[i][j]) * g.alpha);
+      if (fold > 1) {
+        if (m_ok(gm)) C[(gm / g.M) * g.c_bs + gn * g.c_ns + gm % g.M] = c;
+      } else if (gm < g.M) {
+        C[gn * g.c_ns + gm] = c;
+      }
+    }
+  }
+}
+
+template <int TI, int TJ>
+static void launch3m(dim3 grid, const GemmArgs& g, cudaStream_t s) {
+  cudaFuncSetAttribute(cgemm3m_modes_kernel<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)cgemm3m_smem<TI, TJ>());
+  cgemm3m_modes_kernel<TI, TJ><<<grid, 256, cgemm3m_smem<TI, TJ>(), s>>>(g);
+}
+
+static int gemm_algo() {  // TFNO_CGEMM_ALGO: 4 = classic 4M product (default), 3 = Gauss 3M
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFNO_CGEMM_ALGO");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
+static bool big_tiles() {  // TFNO_CGEMM_BIG=0 selects the 64 x 128 tile (A/B runs)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFNO_CGEMM_BIG");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   const bool fast = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) &&
                     (g.w_ks % 2 == 0) && (g.w_bs % 2 == 0) && g.N > 16 && g.M >= 64 &&
@@ -291,15 +451,27 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   const bool foldable = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.M >= 2 && g.M < FBMf &&
                         (FBMf % g.M == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) && (g.w_ks % 2 == 0) &&
                         ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.W % 16 == 0) && g.N > 16;
+  const bool g3 = gemm_algo() == 3;
   if (foldable) {
     GemmArgs f = g;
     f.fold = FBMf / g.M;
     dim3 grid(1u, (unsigned)((g.N + (wide ? 127 : 63)) / (wide ? 128 : 64)),
               (unsigned)((g.batch + f.fold - 1) / f.fold));
-    if (wide)
+    if (g3)
+      wide ? launch3m<4, 8>(grid, f, s) : launch3m<8, 4>(grid, f, s);
+    else if (wide)
       cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(f);
     else
       cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(f);
+  } else if (fast && g.N > 64 && g3) {
+    dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
+    launch3m<4, 8>(grid, g, s);
+  } else if (fast && g.M >= 128 && g3) {
+    dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
+    launch3m<8, 4>(grid, g, s);
+  } else if (fast && g.N > 64 && g.M >= 128 && big_tiles()) {
+    dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
+    cgemm_modes_kernel<8, 8><<<grid, 256, 0, s>>>(g);
   } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);

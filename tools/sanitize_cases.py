@@ -24,7 +24,10 @@ cases = [((1, 2, 2, 128, 128, 16, 16, 2), ["fully_fused"]),            # plane2d
          ((2, 8, 8, 1, 1024, 1, 128, 1), ["fully_fused", "fft_optimized"]),  # warp fused / warp rows
          ((3, 8, 8, 1, 256, 1, 32, 1), ["fully_fused", "fft_optimized"]),
          ((1, 4, 4, 1, 4096, 1, 512, 1), ["fully_fused"]),               # team rows
-         ((2, 8, 8, 1, 128, 1, 32, 1), ["fully_fused", "fused_fft_gemm", "fused_gemm_ifft"])]  # CT rows fused
+         ((2, 8, 8, 1, 128, 1, 32, 1), ["fully_fused", "fused_fft_gemm", "fused_gemm_ifft"]),  # CT rows fused
+         ((3, 64, 64, 1, 256, 1, 32, 1), ["fully_fused"]),               # fused1d, output-channel split 2
+         ((200, 32, 64, 1, 256, 1, 32, 1), ["fully_fused"]),             # fused1d, several items per CTA
+         ((150, 16, 64, 1, 1024, 1, 128, 1), ["fully_fused"])]           # fused1d L = 32
 for shape, modes in cases:
     cfg = T.FnoLayerConfig(*shape)
     x, w = rnd(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), rnd(cfg.hidden_dim, cfg.output_dim)

@@ -157,6 +157,16 @@ struct Sched {
   std::string desc;
 };
 
+int num_sms_api() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
 Sched make_sched(const tfno_cfg* c, int mode) {
   Sched s;
   Geo g = geo_of(c);
@@ -204,6 +214,18 @@ Sched make_sched(const tfno_cfg* c, int mode) {
     // fused only while the C tile covers all of N (else the FFT would be
     // recomputed per n-tile): otherwise the unfused schedule of fast kernels
     ok = (g.N + NT - 1) / NT <= 1;  // measured: a second n-tile (recomputed FFTs) loses to the unfused schedule
+    // ...except when there are too few row groups to fill the SMs (C1: 16):
+    // then split N into tiles so G * tiles approaches one wave (FFT recompute
+    // is cheap next to the idle SMs)
+    const int64_t G = g.B * g.kx;
+    const int sms = num_sms_api();
+    if (ok && 2 * G <= sms) {
+      int tiles = (int)(sms / G);
+      int nt = (int)((g.N + tiles - 1) / tiles);
+      nt = ((nt + 3) / 4) * 4;
+      if (nt < 4) nt = 4;
+      if (nt < NT) NT = nt;
+    }
     s.rows_fast = ok;
     s.rows_NT = NT;
   } else {

@@ -32,27 +32,31 @@
 
 namespace tfno {
 
-template <int L, int KP, int TI, int TJ, int NOUT>
+template <int L, int V, int KP, int TI, int TJ, int NOUT>
 struct F1Geo {
-  static constexpr int N = L * L, NFT = 256, NGT = 256, TEAMS = NFT / L, KC = TEAMS, KT = KP * L;
+  // N = L * V: L lanes per row team, V values per lane (V = L: square rows N = 256 / 1024;
+  // V = 8 with L = 16: N = 128)
+  static constexpr int N = L * V, NFT = 256, NGT = 256, TEAMS = NFT / L, KC = TEAMS, KT = KP * L;
   static constexpr int NTH = NFT + NGT + 128;  // + one producer warpgroup (3 warps idle)
   static constexpr int NA = 2;                 // A chunk ring depth
   static constexpr int MT = KT / TI, NTG = NOUT / TJ;
   static_assert(MT * NTG == NGT, "GEMM thread grid must cover the GEMM warps");
   static_assert(NOUT % TEAMS == 0, "inverse rows per team");
-  static constexpr int BAR_BYTES = 1024;
+  static constexpr int BAR_BYTES = 2048;  // >= 8 * (2 * TEAMS * NSLOT + 2 + 2 + 2 * NA + 2)
   // float2 units after the barrier block; NSLOT input-row slots per team
   static constexpr size_t total(int ns) {
-    return (size_t)TEAMS * N * ns + 2 * KC * NOUT + NA * KC * KT + KT * NOUT + TEAMS * L * L + L * L + L;
+    return (size_t)TEAMS * N * ns + 2 * KC * NOUT + NA * KC * KT + KT * NOUT + TEAMS * N + N + L;
   }
-  static constexpr int NSLOT = (BAR_BYTES + 8 * total(2) <= 220 * 1024) ? 2 : 1;  // deeper prefetch if it fits
+  // input-row slots per team: as deep a prefetch as fits (4 rows in flight per team at N <= 256)
+  static constexpr int NSLOT = (BAR_BYTES + 8 * total(4) <= 220 * 1024) ? 4 : (BAR_BYTES + 8 * total(2) <= 220 * 1024) ? 2 : 1;
+  static_assert(8 * (2 * TEAMS * NSLOT + 4 + 2 * NA + 2) <= BAR_BYTES, "mbarrier block");
   static constexpr int OFF_SLOT = 0;
   static constexpr int OFF_W = OFF_SLOT + TEAMS * N * NSLOT;
   static constexpr int OFF_A = OFF_W + 2 * KC * NOUT;
   static constexpr int OFF_C = OFF_A + NA * KC * KT;
   static constexpr int OFF_TR = OFF_C + KT * NOUT;
-  static constexpr int OFF_TWN = OFF_TR + TEAMS * L * L;
-  static constexpr int OFF_TWL = OFF_TWN + L * L;
+  static constexpr int OFF_TWN = OFF_TR + TEAMS * N;
+  static constexpr int OFF_TWL = OFF_TWN + N;
   static constexpr int TOTAL = OFF_TWL + L;
   static constexpr size_t smem_bytes() { return BAR_BYTES + sizeof(float2) * (size_t)TOTAL; }
   // register split (setmaxnreg) inside the CTA's launch allocation of 640 x 96:
@@ -68,10 +72,14 @@ template <int L>
 __device__ __forceinline__ int tsw(int r, int c) {
   return r * L + (c ^ r);
 }
+// 8 x 16 tile of the N = 128 rows ([k1][t]): the column is XOR-ed with 2*k1 so
+// the row writes (16 consecutive t) and the (k1 = lane/2, t = lane%2 + 2t')
+// reads of a half warp are both conflict free.
+__device__ __forceinline__ int tsw8(int r, int c) { return r * 16 + (c ^ (2 * r)); }
 
-template <int L, int KP, int TI, int TJ, int NOUT>
+template <int L, int V, int KP, int TI, int TJ, int NOUT>
 __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
-  using G = F1Geo<L, KP, TI, TJ, NOUT>;
+  using G = F1Geo<L, V, KP, TI, TJ, NOUT>;
   constexpr int N = G::N, TEAMS = G::TEAMS, KC = G::KC, KT = G::KT, MT = G::MT, NTG = G::NTG, NA = G::NA;
   constexpr int NGW = G::NGT / 32, NS = G::NSLOT;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -98,7 +106,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   const int S = a.nsplit > 1 ? a.nsplit : 1;  // items = row groups x output-channel splits
   const int64_t items = a.G * S;
   for (int k = tid; k < L; k += blockDim.x) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
-  for (int i = tid; i < L * L; i += blockDim.x) {
+  for (int i = tid; i < N; i += blockDim.x) {  // [k1][t] = w_N^{t k1}, k1 < V, t < L
     const int k1 = i / L, t = i % L;
     twN[i] = __ldg(&a.twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
   }
@@ -216,7 +224,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;  // grid <= items
   const int lane = tid % L, team = tid / L;
   const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));
-  float2* trr = tr + team * L * L;
+  float2* trr = tr + team * N;
   int64_t kk = 0;
   for (int64_t it = 0; it <= nmine; ++it) {
     if (it < nmine) {
@@ -225,6 +233,8 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         const int b = team * NS + (int)(kk % NS);
         mbar_wait(&full[b], (uint32_t)((kk / NS) & 1));
         const float2* slot = slots + b * N;
+        const int s = (int)(kk % NA);  // A chunk slot
+        if constexpr (V == L) {
         float2 v[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) v[j] = slot[lane + L * j];
@@ -241,13 +251,51 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         __syncwarp(tmask);
         float2 o[KP];
         wf::dftL_first<L, KP>(v, o, twL);
-        const int s = (int)(kk % NA);
         if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
         float2* Ab = As + s * KC * KT;
 #pragma unroll
         for (int k2 = 0; k2 < KP; ++k2) {
           const int q = lane + L * k2;
           Ab[team * KT + q] = q < keep ? o[k2] : make_float2(0.f, 0.f);
+        }
+        } else {
+        // N = 128 = 16 lanes x 8: Y_t[k1] = DFT8_j x[t + 16 j] * w_128^{t k1};
+        // X[k1 + 8 k2] = sum over t = hf + 2 t' of w_16^{hf k2} DFT8_t'(Y)[k2],
+        // lane = (k1, hf): the two halves are summed with one shuffle.
+        static_assert(V == 8 && L == 16, "row shape");
+        constexpr int K2 = 2 * KP;  // bins k1 + 8 k2 < KT
+        float2 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = slot[lane + 16 * j];
+        __syncwarp(tmask);
+        if (lane == 0) mbar_arrive(&empty[b]);
+        dft8<-1>(v);
+#pragma unroll
+        for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], twN[k1 * 16 + lane]);
+#pragma unroll
+        for (int k1 = 0; k1 < 8; ++k1) trr[tsw8(k1, lane)] = v[k1];
+        __syncwarp(tmask);
+        const int k1 = lane >> 1, hf = lane & 1;
+#pragma unroll
+        for (int t2 = 0; t2 < 8; ++t2) v[t2] = trr[tsw8(k1, hf + 2 * t2)];
+        __syncwarp(tmask);
+        dft8<-1>(v);
+#pragma unroll
+        for (int k2 = 1; k2 < K2; ++k2)
+          if (hf) v[k2] = cmul(v[k2], twL[k2]);
+#pragma unroll
+        for (int k2 = 0; k2 < K2; ++k2) {
+          const float2 p = make_float2(__shfl_xor_sync(tmask, v[k2].x, 1), __shfl_xor_sync(tmask, v[k2].y, 1));
+          v[k2] = cadd(v[k2], p);
+        }
+        if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
+        float2* Ab = As + s * KC * KT;
+#pragma unroll
+        for (int k2 = 0; k2 < K2; ++k2) {
+          if ((k2 & 1) != hf) continue;
+          const int q = k1 + 8 * k2;
+          Ab[team * KT + q] = q < keep ? v[k2] : make_float2(0.f, 0.f);
+        }
         }
         __syncwarp(tmask);
         if (lane == 0) mbar_arrive(&afull[s]);
@@ -261,6 +309,8 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
       float2* yg = a.y + bb * a.y_sb + pp * a.y_sp + n0 * a.y_sn;
       mbar_wait(cfull, (uint32_t)((it - 1) & 1));
       for (int n = team; n < NOUT; n += TEAMS) {
+        float2* dst = yg + (int64_t)n * a.y_sn;
+        if constexpr (V == L) {
         float2 xk[KP];
 #pragma unroll
         for (int k2 = 0; k2 < KP; ++k2) {
@@ -278,9 +328,35 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         for (int k1 = 0; k1 < L; ++k1) z[k1] = trr[tsw<L>(lane, k1)];
         __syncwarp(tmask);
         wf::dftL<L, 1>(z, twL);
-        float2* dst = yg + (int64_t)n * a.y_sn;
 #pragma unroll
         for (int j = 0; j < L; ++j) __stcs(dst + lane + L * j, cscale(z[j], a.inv_scale));
+        } else {
+        // N = 128: lane (k1, hf) forms Y_t[k1] for t = hf + 2 t' from its
+        // nonzero bins X[k1 + 8 k2], twiddles by w_128^{+k1 t}, transposes;
+        // lane t then runs the inverse DFT8 over k1 -> y[t + 16 j]
+        constexpr int K2 = 2 * KP;
+        const int k1 = lane >> 1, hf = lane & 1;
+        float2 z[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const int q = k1 + 8 * k2;
+          z[k2] = (k2 < K2 && q < keep) ? Cs[n * KT + q] : make_float2(0.f, 0.f);
+          if (k2 < K2 && k2 && hf) z[k2] = cmul(z[k2], conjf2(twL[k2]));
+        }
+        dft8<1>(z);
+#pragma unroll
+        for (int t2 = 0; t2 < 8; ++t2) {
+          const int t = hf + 2 * t2;
+          trr[tsw8(k1, t)] = k1 ? cmul(z[t2], conjf2(twN[k1 * 16 + t])) : z[t2];
+        }
+        __syncwarp(tmask);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) z[r] = trr[tsw8(r, lane)];
+        __syncwarp(tmask);
+        dft8<1>(z);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) __stcs(dst + lane + 16 * j, cscale(z[j], a.inv_scale));
+        }
       }
       __syncwarp(tmask);
       if (lane == 0) mbar_arrive(cempty);
@@ -290,37 +366,39 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 
 // ---------------------------------------------------------------- dispatch
 struct F1Shape {
-  int L, KP, TI, TJ, NOUT;
+  int L, V, KP, TI, TJ, NOUT;
 };
 // instantiated shapes: keep <= KP*L (masked), H % (256/L) == 0, N_out == NOUT
 static const F1Shape kF1Shapes[] = {
-    {16, 1, 1, 4, 64}, {16, 1, 1, 8, 128}, {16, 1, 2, 8, 256},  // keep <= 16 (N = 256)
-    {16, 2, 1, 4, 32},                                          // keep <= 32, N_out (per split) 32
-    {16, 2, 2, 4, 64}, {16, 2, 2, 8, 128}, {16, 2, 4, 8, 256},  // keep <= 32
-    {16, 4, 4, 4, 64}, {16, 4, 4, 8, 128},                      // keep <= 64
-    {32, 2, 4, 4, 64},                                          // keep <= 64 (N = 1024)
-    {32, 4, 8, 4, 64},                                          // keep <= 128
+    {16, 16, 1, 1, 4, 64}, {16, 16, 1, 1, 8, 128}, {16, 16, 1, 2, 8, 256},  // keep <= 16 (N = 256)
+    {16, 16, 2, 1, 4, 32},                                                  // keep <= 32, N_out (per split) 32
+    {16, 16, 2, 2, 4, 64}, {16, 16, 2, 2, 8, 128}, {16, 16, 2, 4, 8, 256},  // keep <= 32
+    {16, 16, 4, 4, 4, 64}, {16, 16, 4, 4, 8, 128},                          // keep <= 64
+    {32, 32, 2, 4, 4, 64},                                                  // keep <= 64 (N = 1024)
+    {32, 32, 4, 8, 4, 64},                                                  // keep <= 128
+    {16, 8, 2, 1, 2, 16}, {16, 8, 2, 1, 4, 32}, {16, 8, 2, 2, 4, 64},      // N = 128, keep <= 32 (C1)
 };
 
 static const F1Shape* f1_pick(int n, int keep, int H, int NO) {
-  const int L = n == 256 ? 16 : (n == 1024 ? 32 : 0);
+  const int L = (n == 256 || n == 128) ? 16 : (n == 1024 ? 32 : 0);
+  const int V = n == 128 ? 8 : L;
   if (!L || keep < 1 || H < 1 || H % (256 / L) != 0) return nullptr;
   const int kp = (keep + L - 1) / L;
   for (const F1Shape& s : kF1Shapes)
-    if (s.L == L && s.NOUT == NO && (s.KP == kp || (kp == 3 && s.KP == 4))) return &s;
+    if (s.L == L && s.V == V && s.NOUT == NO && (s.KP == kp || (kp == 3 && s.KP == 4))) return &s;
   return nullptr;
 }
 
 bool fused1d_supported(int n, int keep, int H, int NO) { return f1_pick(n, keep, H, NO) != nullptr; }
 
-template <int L, int KP, int TI, int TJ, int NOUT>
+template <int L, int V, int KP, int TI, int TJ, int NOUT>
 static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
-  using G = F1Geo<L, KP, TI, TJ, NOUT>;
+  using G = F1Geo<L, V, KP, TI, TJ, NOUT>;
   static_assert(G::smem_bytes() <= 227 * 1024, "shared memory");
   const size_t smem = G::smem_bytes();
   if ((uintptr_t)a.x % 16 || (uintptr_t)a.W % 16 || (a.x_sh % 2) || (a.x_sb % 2) || (a.x_sp % 2))
     return cudaErrorNotSupported;  // TMA bulk copies need 16-byte aligned rows
-  cudaError_t e = cudaFuncSetAttribute(fused1d_kernel<L, KP, TI, TJ, NOUT>,
+  cudaError_t e = cudaFuncSetAttribute(fused1d_kernel<L, V, KP, TI, TJ, NOUT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -329,7 +407,7 @@ static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
   const int64_t items = a.G * (a.nsplit > 1 ? a.nsplit : 1);
   const int grid = (int)(items < sms ? items : sms);
   if (grid < 1) return cudaSuccess;
-  fused1d_kernel<L, KP, TI, TJ, NOUT><<<grid, G::NTH, smem, s>>>(a);
+  fused1d_kernel<L, V, KP, TI, TJ, NOUT><<<grid, G::NTH, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -349,14 +427,15 @@ cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s) {
   if (a.N % S) return cudaErrorNotSupported;
   const F1Shape* p = f1_pick(a.n, a.keep, a.H, a.N / S);
   if (!p) return cudaErrorNotSupported;
-#define F1_CASE(LL, KK, TI_, TJ_, NO_) \
-  if (p->L == LL && p->KP == KK && p->NOUT == NO_) return launch_f1<LL, KK, TI_, TJ_, NO_>(a, s);
-  F1_CASE(16, 1, 1, 4, 64) F1_CASE(16, 1, 1, 8, 128) F1_CASE(16, 1, 2, 8, 256)
-  F1_CASE(16, 2, 1, 4, 32)
-  F1_CASE(16, 2, 2, 4, 64) F1_CASE(16, 2, 2, 8, 128) F1_CASE(16, 2, 4, 8, 256)
-  F1_CASE(16, 4, 4, 4, 64) F1_CASE(16, 4, 4, 8, 128)
-  F1_CASE(32, 2, 4, 4, 64)
-  F1_CASE(32, 4, 8, 4, 64)
+#define F1_CASE(LL, VV, KK, TI_, TJ_, NO_) \
+  if (p->L == LL && p->V == VV && p->KP == KK && p->NOUT == NO_) return launch_f1<LL, VV, KK, TI_, TJ_, NO_>(a, s);
+  F1_CASE(16, 16, 1, 1, 4, 64) F1_CASE(16, 16, 1, 1, 8, 128) F1_CASE(16, 16, 1, 2, 8, 256)
+  F1_CASE(16, 16, 2, 1, 4, 32)
+  F1_CASE(16, 16, 2, 2, 4, 64) F1_CASE(16, 16, 2, 2, 8, 128) F1_CASE(16, 16, 2, 4, 8, 256)
+  F1_CASE(16, 16, 4, 4, 4, 64) F1_CASE(16, 16, 4, 4, 8, 128)
+  F1_CASE(32, 32, 2, 4, 4, 64)
+  F1_CASE(32, 32, 4, 8, 4, 64)
+  F1_CASE(16, 8, 2, 1, 2, 16) F1_CASE(16, 8, 2, 1, 4, 32) F1_CASE(16, 8, 2, 2, 4, 64)
 #undef F1_CASE
   return cudaErrorNotSupported;
 }

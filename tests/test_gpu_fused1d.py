@@ -39,6 +39,8 @@ CASES = [
     (2, 32, 64, 1, 256, 1, 20, 1),       # ragged keep (masked bins), H = 2 chunks
     (2, 128, 64, 1, 256, 1, 50, 1),      # keep 50 -> KP = 4 tile
     (2, 64, 64, 4, 256, 2, 32, 2),       # rank 2: x passes around the fused rows
+    (16, 64, 64, 1, 128, 1, 32, 1),      # C1 exactly: N = 128 rows (16 lanes x 8), split 4
+    (3, 32, 64, 1, 128, 1, 20, 1),       # N = 128, ragged keep
 ]
 
 
@@ -59,7 +61,7 @@ def test_fused1d_vs_oracle(T, O, case):
     assert T.max_rel_error(out.data, exact) < FP32_TOL
 
 
-@pytest.mark.parametrize("n,h,keep", [(256, 64, 32), (256, 256, 32), (1024, 64, 128)])
+@pytest.mark.parametrize("n,h,keep", [(256, 64, 32), (256, 256, 32), (1024, 64, 128), (128, 64, 32)])
 def test_fused1d_many_items_vs_unfused(T, n, h, keep):
     """Batch >> #SMs (several items per persistent CTA, ring phases wrap):
     fused == unfused schedule within FP32 tolerance, and deterministic."""

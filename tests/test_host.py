@@ -111,7 +111,12 @@ def test_schedules_and_workspace():
     assert T.layer_schedule(c4, "fully_fused") == (3, "plane-fft2d|cgemm-modes|plane-ifft2d")
     assert T.workspace_bytes(c4, "fully_fused") == 2 * 128 * 128 * 64 * 64 * 8
     c1 = T.FnoLayerConfig(16, 64, 64, 1, 128, 1, 32, 1)
-    assert T.layer_schedule(c1, "fully_fused") == (1, "fused-fft-cgemm-ifft")
+    assert T.layer_schedule(c1, "fully_fused") == (1, "fused1d-fft-cgemm-ifft")  # one launch (fused1d.cu)
+    assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused-fft-cgemm|y-ifft")
+    c2 = T.FnoLayerConfig(1024, 256, 256, 1, 256, 1, 32, 1)
+    assert T.layer_schedule(c2, "fully_fused") == (1, "fused1d-fft-cgemm-ifft")
+    c2b = T.FnoLayerConfig(1024, 256, 256, 1, 4096, 1, 512, 1)
+    assert T.layer_schedule(c2b, "fully_fused") == (3, "y-fft|cgemm|y-ifft")
     assert T.layer_schedule(c1, "fft_optimized")[0] == 3
     r2 = T.FnoLayerConfig(2, 16, 16, 32, 64, 8, 16, 2)
     assert T.layer_schedule(r2, "fully_fused") == (3, "x-fft|fused-fft-cgemm-ifft|x-ifft")

@@ -286,24 +286,43 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
 // Gauss / 3M variant of the mode CGEMM: a complex MAC in 3 real FFMAs
 // instead of 4.  With s = ar + ai, d = wi - wr, u = wr + wi:
 //   t1 += s*wr,  t2 += ar*d,  t3 += ai*u;   Re C = t1 - t3,  Im C = t1 + t2.
-// The sums are formed once per element when a chunk is staged into shared
-// memory (A as (ar, ai, s), W as (wr, d, u), float4 each), so the inner loop
-// is TI + TJ LDS.128 per 3*TI*TJ FFMA.  Same FP32 arithmetic, 25% fewer FMA
-// issues than cgemm.gemm_kloop's 4M product; error stays at fp32 level
-// (tests/test_gpu_parity.py: <= 1e-5 vs float64, like the 4M kernel).
-// Measured SLOWER on B200 (N1024 H256: 1.92 vs 1.46 ms, ncu: 47% issue, the
-// register prefetch of A is sunk by ptxas at 253 registers -> long-scoreboard
-// stalls), so it is opt-in (TFNO_CGEMM_ALGO=3); profiles/r01/cgemm_3m_vs_4m.txt.
+// Raw (ar, ai) / (wr, wi) chunks stream global -> shared with cp.async
+// (3 stages, no prefetch registers); once a chunk has landed the CTA rewrites
+// it as float4 (ar, ai, s) / (wr, d, u) into a double-buffered compute tile,
+// so the inner loop is TI + TJ LDS.128 per 3*TI*TJ FFMA (4M: TI + TJ LDS.64
+// per 4*TI*TJ).  Same FP32 arithmetic as cgemm.gemm_kloop up to rounding of
+// the sums; tests/test_gpu_parity.py holds it to 1e-5 vs float64.
+// 16-byte cp.async; bytes < 16 copies the first `bytes` and zero-fills the rest
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int TI, int TJ>
+struct G3 {
+  static constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = 16, NST = 3;
+  // float4 units: raw stages hold complex pairs, compute tiles hold one complex + sum
+  static constexpr int RAW = FBK * (FBM + FBN) / 2;
+  static constexpr int TILE = FBK * (FBM + FBN);
+  static constexpr size_t smem() { return sizeof(float4) * ((size_t)NST * RAW + 2 * (size_t)TILE); }
+};
 template <int TI, int TJ>
 constexpr size_t cgemm3m_smem() {
-  return sizeof(float4) * 2 * 16 * (16 * TI + 16 * TJ);
+  return G3<TI, TJ>::smem();
 }
+
 template <int TI, int TJ>
 __global__ void __launch_bounds__(256, 1) cgemm3m_modes_kernel(GemmArgs g) {
-  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = 16;
+  using Q = G3<TI, TJ>;
+  constexpr int FBM = Q::FBM, FBN = Q::FBN, FBK = Q::FBK, NST = Q::NST;
   extern __shared__ __align__(16) float4 sm3[];
-  float4 (*As)[FBK][FBM] = reinterpret_cast<float4 (*)[FBK][FBM]>(sm3);
-  float4 (*Ws)[FBK][FBN] = reinterpret_cast<float4 (*)[FBK][FBN]>(sm3 + 2 * FBK * FBM);
+  float4* raw = sm3;                         // [NST][FBK*FBM/2 (A pairs) + FBK*FBN/2 (W pairs)]
+  float4* tile = sm3 + NST * Q::RAW;         // [2][FBK*FBM (A) + FBK*FBN (W)]
   const int tid = threadIdx.x;
   const int tm = tid % 16, tn = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
@@ -313,54 +332,42 @@ __global__ void __launch_bounds__(256, 1) cgemm3m_modes_kernel(GemmArgs g) {
   const float2* __restrict__ W = g.W + (fold > 1 ? 0 : b * g.w_bs);
   auto a_off = [&](int64_t gm) -> int64_t { return fold > 1 ? (gm / g.M) * g.a_bs + gm % g.M : gm; };
   auto m_ok = [&](int64_t gm) { return fold > 1 ? (gm / g.M < fold && b + gm / g.M < g.batch) : gm < g.M; };
-  constexpr int NA = FBK * FBM / 2 / 256, NW = FBK * FBN / 2 / 256;  // float4 (complex pairs) per thread
-  static_assert(NA >= 1 && NW >= 1, "tile");
-  float4 ra[NA], rw[NW];
-  auto load_chunk = [&](int64_t k0) {
+  constexpr int PA = FBK * FBM / 2, PW = FBK * FBN / 2;  // 16-byte pieces per chunk
+  const int nch = (int)((g.K + FBK - 1) / FBK);
+  auto issue = [&](int st, int64_t k0) {
+    float4* ra = raw + st * Q::RAW;
+    float4* rw = ra + PA;
 #pragma unroll
-    for (int r = 0; r < NA; ++r) {
-      const int i = tid + r * 256;
+    for (int i = tid; i < PA; i += 256) {
       const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
       const int64_t gk = k0 + kk, gm = m0 + mm;
-      if (fold > 1) {
-        ra[r] = (gk < g.K && m_ok(gm)) ? __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + a_off(gm)))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if (gk < g.K && gm + 1 < g.M) {
-        ra[r] = __ldg(reinterpret_cast<const float4*>(A + gk * g.a_ks + gm));
-      } else {
-        float2 v0 = (gk < g.K && gm < g.M) ? A[gk * g.a_ks + gm] : make_float2(0.f, 0.f);
-        ra[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
-      }
+      const int nb = gk >= g.K ? 0 : fold > 1 ? (m_ok(gm) ? 16 : 0) : (gm + 1 < g.M ? 16 : gm < g.M ? 8 : 0);
+      cp_async16(ra + i, nb ? (const void*)(A + gk * g.a_ks + a_off(gm)) : (const void*)A, nb);
     }
 #pragma unroll
-    for (int r = 0; r < NW; ++r) {
-      const int i = tid + r * 256;
+    for (int i = tid; i < PW; i += 256) {
       const int kk = i / (FBN / 2), nn = (i % (FBN / 2)) * 2;
       const int64_t gk = k0 + kk, gn = n0 + nn;
-      if (gk < g.K && gn + 1 < g.N) {
-        rw[r] = __ldg(reinterpret_cast<const float4*>(W + gk * g.w_ks + gn));
-      } else {
-        float2 v0 = (gk < g.K && gn < g.N) ? W[gk * g.w_ks + gn] : make_float2(0.f, 0.f);
-        rw[r] = make_float4(v0.x, v0.y, 0.f, 0.f);
-      }
+      const int nb = gk >= g.K ? 0 : (gn + 1 < g.N ? 16 : gn < g.N ? 8 : 0);
+      cp_async16(rw + i, nb ? (const void*)(W + gk * g.w_ks + gn) : (const void*)W, nb);
     }
   };
-  auto store_chunk = [&](int buf) {
+  auto transform = [&](int st, int tb) {
+    const float4* ra = raw + st * Q::RAW;
+    const float4* rw = ra + PA;
+    float4* ta = tile + tb * Q::TILE;
+    float4* tw = ta + FBK * FBM;
 #pragma unroll
-    for (int r = 0; r < NA; ++r) {
-      const int i = tid + r * 256;
-      const int kk = i / (FBM / 2), mm = (i % (FBM / 2)) * 2;
-      const float4 v = ra[r];
-      As[buf][kk][mm] = make_float4(v.x, v.y, v.x + v.y, 0.f);
-      As[buf][kk][mm + 1] = make_float4(v.z, v.w, v.z + v.w, 0.f);
+    for (int i = tid; i < PA; i += 256) {
+      const float4 v = ra[i];
+      ta[2 * i] = make_float4(v.x, v.y, v.x + v.y, 0.f);
+      ta[2 * i + 1] = make_float4(v.z, v.w, v.z + v.w, 0.f);
     }
 #pragma unroll
-    for (int r = 0; r < NW; ++r) {
-      const int i = tid + r * 256;
-      const int kk = i / (FBN / 2), nn = (i % (FBN / 2)) * 2;
-      const float4 v = rw[r];
-      Ws[buf][kk][nn] = make_float4(v.x, v.y - v.x, v.x + v.y, 0.f);
-      Ws[buf][kk][nn + 1] = make_float4(v.z, v.w - v.z, v.z + v.w, 0.f);
+    for (int i = tid; i < PW; i += 256) {
+      const float4 v = rw[i];
+      tw[2 * i] = make_float4(v.x, v.y - v.x, v.x + v.y, 0.f);
+      tw[2 * i + 1] = make_float4(v.z, v.w - v.z, v.z + v.w, 0.f);
     }
   };
   float t1[TI][TJ], t2[TI][TJ], t3[TI][TJ];
@@ -368,20 +375,26 @@ __global__ void __launch_bounds__(256, 1) cgemm3m_modes_kernel(GemmArgs g) {
   for (int i = 0; i < TI; ++i)
 #pragma unroll
     for (int j = 0; j < TJ; ++j) t1[i][j] = t2[i][j] = t3[i][j] = 0.f;
-  load_chunk(0);
-  store_chunk(0);
+  issue(0, 0);
+  cp_async_commit();
+  if (nch > 1) issue(1, FBK);
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncthreads();
-  int buf = 0;
-  for (int64_t k0 = 0; k0 < g.K; k0 += FBK) {
-    const bool more = k0 + FBK < g.K;
-    if (more) load_chunk(k0 + FBK);
+  transform(0, 0);
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    if (c + 2 < nch) issue((c + 2) % NST, (int64_t)(c + 2) * FBK);
+    cp_async_commit();  // (possibly empty) group c + 2 keeps the wait counts uniform
+    const float4* ta = tile + (c & 1) * Q::TILE;
+    const float4* tw = ta + FBK * FBM;
 #pragma unroll
     for (int kk = 0; kk < FBK; ++kk) {
       float4 av[TI], bv[TJ];
 #pragma unroll
-      for (int i = 0; i < TI; ++i) av[i] = As[buf][kk][tm + 16 * i];
+      for (int i = 0; i < TI; ++i) av[i] = ta[kk * FBM + tm + 16 * i];
 #pragma unroll
-      for (int j = 0; j < TJ; ++j) bv[j] = Ws[buf][kk][tn + 16 * j];
+      for (int j = 0; j < TJ; ++j) bv[j] = tw[kk * FBN + tn + 16 * j];
 #pragma unroll
       for (int i = 0; i < TI; ++i)
 #pragma unroll
@@ -391,10 +404,11 @@ __global__ void __launch_bounds__(256, 1) cgemm3m_modes_kernel(GemmArgs g) {
           t3[i][j] = fmaf(av[i].y, bv[j].z, t3[i][j]);
         }
     }
-    if (more) {
-      store_chunk(buf ^ 1);  // last read in the previous chunk, before its barrier
+    if (c + 1 < nch) {
+      cp_async_wait<1>();  // chunk c + 1 has landed (this thread's pieces)
+      __syncthreads();     // ... everyone's, and everyone is done with tile (c + 1) & 1's old data
+      transform((c + 1) % NST, (c + 1) & 1);
       __syncthreads();
-      buf ^= 1;
     }
   }
   float2* C = g.C + b * g.c_bs;
@@ -422,13 +436,9 @@ static void launch3m(dim3 grid, const GemmArgs& g, cudaStream_t s) {
   cgemm3m_modes_kernel<TI, TJ><<<grid, 256, cgemm3m_smem<TI, TJ>(), s>>>(g);
 }
 
-static int gemm_algo() {  // TFNO_CGEMM_ALGO: 4 = classic 4M product (default), 3 = Gauss 3M
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TFNO_CGEMM_ALGO");
-    v = e ? atoi(e) : 4;
-  }
-  return v;
+static int gemm_algo() {  // TFNO_CGEMM_ALGO: 4 = classic 4M product (default), 3 = Gauss 3M (read per call)
+  const char* e = getenv("TFNO_CGEMM_ALGO");
+  return e ? atoi(e) : 4;
 }
 
 static bool big_tiles() {  // TFNO_CGEMM_BIG=0 selects the 64 x 128 tile (A/B runs)

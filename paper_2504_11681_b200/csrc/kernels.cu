@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
 // so the inner loop is TI + TJ LDS.128 per 3*TI*TJ FFMA (4M: TI + TJ LDS.64
 // per 4*TI*TJ).  Same FP32 arithmetic as cgemm.gemm_kloop up to rounding of
 // the sums; tests/test_gpu_parity.py holds it to 1e-5 vs float64.
+// Measured on B200 (N1024 H256 B1024): 1.70 ms vs 1.46 ms for the 4M 8x8 tile:
+// 20% fewer instructions but 56% issue (short-scoreboard on the LDS.128
+// operands with one 8-warp CTA per SM), so it stays opt-in
+// (TFNO_CGEMM_ALGO=3); profiles/r01/cgemm_3m_vs_4m.txt.
 // 16-byte cp.async; bytes < 16 copies the first `bytes` and zero-fills the rest
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int bytes) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);

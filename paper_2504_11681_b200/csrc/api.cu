@@ -167,7 +167,7 @@ int num_sms_api() {
   return n;
 }
 
-Sched make_sched(const tfno_cfg* c, int mode) {
+Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
   Sched s;
   Geo g = geo_of(c);
   if (mode == TFNO_STAGED) {
@@ -193,7 +193,11 @@ Sched make_sched(const tfno_cfg* c, int mode) {
     const char* e = getenv("TFNO_FUSED1D");
     f1_env = e ? atoi(e) : -1;
   }
-  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
+  // tensor-core precisions on contraction-heavy shapes: the fused 1D kernel's
+  // contraction is FP32 SIMT, so the unfused schedule with the tcgen05 CGEMM wins
+  const bool tc_heavy = prec != TFNO_FP32 && g.H * g.N >= 128 * 128;
+  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy &&
+      fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
     s.f1 = true;
     s.f1_split = fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
     s.fg = s.gi = true;
@@ -202,7 +206,7 @@ Sched make_sched(const tfno_cfg* c, int mode) {
     s.desc = g.rank == 2 ? "x-fft|fused1d-fft-cgemm-ifft|x-ifft" : "fused1d-fft-cgemm-ifft";
     return s;
   }
-  if (mode == TFNO_FULLY_FUSED && warp_fused_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
+  if (mode == TFNO_FULLY_FUSED && !tc_heavy && warp_fused_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
     s.warp_fused = true;
     s.fg = s.gi = true;
     s.need_s1 = s.need_mid = (g.rank == 2);
@@ -231,6 +235,7 @@ Sched make_sched(const tfno_cfg* c, int mode) {
   } else {
     ok = fused_tiling((int)g.dy, (int)g.ky, (int)g.N, fa);
   }
+  if (tc_heavy) ok = false;  // the standalone tcgen05 CGEMM beats the fused SIMT contraction
   s.fg = want_fg && ok;
   s.gi = want_gi && ok;
   s.need_s1 = s.need_mid = (g.rank == 2);
@@ -377,9 +382,20 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   return cuda_status(cudaGetLastError());
 }
 
-size_t ws_bytes_for(const tfno_cfg* c, int mode) {
+// the channel mix runs as a standalone CGEMM (plane2d path or the unfused row schedule)
+bool sched_has_cgemm(const Sched& s) { return s.plane2d || (!s.staged && !s.fg && !s.gi); }
+
+size_t wimg_bytes_for(const tfno_cfg* c, int mode, int prec) {
+  Sched s = make_sched(c, mode, prec);
+  if (!sched_has_cgemm(s)) return 0;
   Geo g = geo_of(c);
-  Sched s = make_sched(c, mode);
+  const size_t b = cgemm_tc_wimg_bytes(g.N, g.H, prec);
+  return (b + 255) & ~(size_t)255;
+}
+
+size_t base_ws_bytes(const tfno_cfg* c, int mode, int prec) {  // intermediates only
+  Geo g = geo_of(c);
+  Sched s = make_sched(c, mode, prec);
   if (s.staged) return staged_ws(g);
   size_t e = 0;
   if (s.need_s1) e += g.B * g.H * g.kx * g.dy;
@@ -387,6 +403,10 @@ size_t ws_bytes_for(const tfno_cfg* c, int mode) {
   if (s.need_A) e += g.B * g.H * g.kx * g.ky;
   if (s.need_C) e += g.B * g.N * g.kx * g.ky;
   return e * sizeof(float2);
+}
+
+size_t ws_bytes_for(const tfno_cfg* c, int mode, int prec = 0) {
+  return base_ws_bytes(c, mode, prec) + wimg_bytes_for(c, mode, prec);
 }
 
 FftPencilArgs pencil_args(int n, int keep, int src_len, int64_t P, const float2* in, PencilMap im, float2* out,
@@ -465,20 +485,19 @@ uint32_t tfno_config_violations(const tfno_cfg* c, const tfno_tiles* t, int fft_
 }
 
 size_t tfno_workspace_bytes(const tfno_cfg* c, int mode, int prec) {
-  (void)prec;
   if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
-  return ws_bytes_for(c, mode);
+  return ws_bytes_for(c, mode, prec);
 }
 
 int tfno_layer_schedule(const tfno_cfg* c, int mode, int prec, char* desc, size_t len) {
-  (void)prec;
   if (!c || mode < 0 || mode > 4 || tfno_config_violations(c, nullptr, 8)) return -1;
-  Sched s = make_sched(c, mode);
+  Sched s = make_sched(c, mode, prec);
   if (desc && len) {
     strncpy(desc, s.desc.c_str(), len - 1);
     desc[len - 1] = 0;
   }
-  return s.launches;
+  // the TF32 / 3xTF32 contraction adds one launch building the W' image (same stage)
+  return s.launches + (wimg_bytes_for(c, mode, prec) ? 1 : 0);
 }
 
 int tfno_fft_execute(int n, int direction, int keep, int src_len, int64_t P, const void* in, int64_t in_P0,
@@ -597,10 +616,13 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   const float2* w = (const float2*)wv;
   float2* y = (float2*)yv;
   float2* ws = (float2*)wsv;
-  size_t need = ws_bytes_for(c, mode);
+  // a workspace sized without the W' image (older callers) still works: the
+  // tensor-core contraction then builds W' per CTA
+  size_t need = base_ws_bytes(c, mode, prec);
   if (ws_bytes < need || (need && !ws)) return TFNO_EWORKSPACE;
+  const size_t wimg_need = wimg_bytes_for(c, mode, prec);
   Geo g = geo_of(c);
-  Sched s = make_sched(c, mode);
+  Sched s = make_sched(c, mode, prec);
   if (s.staged) return staged_forward(c, x, w, y, ws, ws_bytes, st);
   int err = 0;
   const float2* tw = twiddle_table(err);
@@ -616,9 +638,10 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   if (s.need_mid) { mid = p; p += g.B * g.N * g.kx * g.dy; }
   if (s.need_A) { A = p; p += g.B * g.H * g.kx * g.ky; }
   if (s.need_C) { Cm = p; p += g.B * g.N * g.kx * g.ky; }
+  void* wimg = (wimg_need && ws_bytes >= need + wimg_need) ? (void*)p : nullptr;
 
   stage_begin(st);
-  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, st, &stage_mark));
+  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, st, &stage_mark));
 
   cudaError_t e;
   const float2* src = x;
@@ -685,6 +708,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     // C[b, n, pq] = sum_h A[b, h, pq] W[h, n]
     GemmArgs ga{g.kx * g.ky, g.N, g.H, g.B, A, 1, g.kx * g.ky, g.H * g.kx * g.ky, w, g.N, 1, 0,
                 Cm, 1, g.kx * g.ky, g.N * g.kx * g.ky, 1.0f};
+    ga.wimg = wimg;
     if (g.B > 65535) return TFNO_EUNSUPPORTED;
     if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e == cudaErrorNotSupported ? TFNO_EUNSUPPORTED : TFNO_ECUDA;
     stage_mark(st);

@@ -139,6 +139,203 @@ __device__ __forceinline__ float4 sub4(float4 a, float4 b) {
   return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
 }
 
+// W' image: for every output-channel block nb and K' chunk c, the B tile(s)
+// exactly as they sit in shared memory (K-major canonical, hi then lo for
+// 3xTF32).  Built once per call by wimg_kernel, then each CTA fetches a
+// chunk with one cp.async.bulk instead of converting W element by element.
+template <int NP, int PASSES>
+__global__ void __launch_bounds__(256) wimg_kernel(GemmArgs g, uint8_t* img) {
+  constexpr int B_LBO = (NP / 8) * 128, BT = TcGeo<NP>::B_TILE, CH = (PASSES > 1 ? 2 : 1) * BT;
+  const int64_t N = g.N, K = g.K;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));
+  const int64_t items = (int64_t)nsplit * nchunks * (NP / 2) * (TC_BK / 4);  // (n, channel pair) items
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+    const int nl = (int)(it % (NP / 2));
+    const int hp = (int)((it / (NP / 2)) % (TC_BK / 4));
+    const int64_t blk = it / ((NP / 2) * (TC_BK / 4));  // nb * nchunks + c
+    const int c = (int)(blk % nchunks);
+    const int64_t nb = blk / nchunks;
+    const int64_t h = (int64_t)c * (TC_BK / 2) + 2 * hp, n = nb * (NP / 2) + nl;
+    const float2 w0 = (n < N && h < K) ? g.W[h * g.w_ks + n] : make_float2(0.f, 0.f);
+    const float2 w1 = (n < N && h + 1 < K) ? g.W[(h + 1) * g.w_ks + n] : make_float2(0.f, 0.f);
+    const float4 re_row = make_float4(w0.x, -w0.y, w1.x, -w1.y);
+    const float4 im_row = make_float4(w0.y, w0.x, w1.y, w1.x);
+    uint8_t* base = img + blk * CH;
+    const uint32_t o0 = cm_off(2 * nl, 4 * hp, B_LBO), o1 = cm_off(2 * nl + 1, 4 * hp, B_LBO);
+    if (PASSES == 1) {
+      *reinterpret_cast<float4*>(base + o0) = re_row;
+      *reinterpret_cast<float4*>(base + o1) = im_row;
+    } else {
+      const float4 h0 = hi4(re_row), h1 = hi4(im_row);
+      *reinterpret_cast<float4*>(base + o0) = h0;
+      *reinterpret_cast<float4*>(base + o1) = h1;
+      *reinterpret_cast<float4*>(base + BT + o0) = sub4(re_row, h0);
+      *reinterpret_cast<float4*>(base + BT + o1) = sub4(im_row, h1);
+    }
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::saddr(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tc::saddr(dst)),
+      "l"(src), "r"(bytes), "r"(tc::saddr(bar))
+      : "memory");
+}
+
+// W'-image variant: 256 threads stage A (two modes per 16-byte load), one
+// thread TMA-copies the chunk's W' tile(s); stage = [A hi | A lo | B hi | B lo].
+template <int NP, int PASSES>
+__global__ void __launch_bounds__(256, 1) cgemm_tc_img_kernel(GemmArgs g) {
+  using Gm = TcGeo<NP>;
+  constexpr int A_LBO = (TC_BM / 8) * 128, B_LBO = (NP / 8) * 128;
+  constexpr int AT = Gm::A_TILE, BT = Gm::B_TILE, NPASS = PASSES > 1 ? 2 : 1;
+  constexpr int STAGE = NPASS * (AT + BT);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);  // [2] MMA done, [2] W' landed
+  uint64_t* wbars = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = g.M, N = g.N, K = g.K;
+  const int mtiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));
+  const int64_t tiles = (int64_t)mtiles * nsplit * g.batch;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);
+  const uint8_t* img = reinterpret_cast<const uint8_t*>(g.wimg);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::saddr(tmem_slot)),
+                 "n"(Gm::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t IDESC = tc::make_idesc(TC_BM, NP, true);
+  // A item = (mode pair, channel pair): A[h][m..m+1], A[h+1][m..m+1] (two float4 loads)
+  // -> K-major rows m and m+1 of (re_h, im_h, re_h+1, im_h+1)
+  constexpr int AI = (TC_BM / 2) * (TC_BK / 4) / 256;  // 2 items per thread
+  float4 ra[AI][2];
+  const bool vec = (M % 2 == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0);
+  auto load_chunk = [&](int64_t tile, int c) {
+    const int64_t b = tile / ((int64_t)mtiles * nsplit);
+    const int64_t m0 = (tile % mtiles) * TC_BM;
+    const int64_t h0 = (int64_t)c * (TC_BK / 2);
+    const float2* Ab = g.A + b * g.a_bs;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 256;
+      const int mp = idx % (TC_BM / 2), hp = idx / (TC_BM / 2);
+      const int64_t m = m0 + 2 * mp, h = h0 + 2 * hp;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t hh = h + r;
+        if (hh < K && m + 1 < M && vec) {
+          ra[i][r] = __ldg(reinterpret_cast<const float4*>(Ab + hh * g.a_ks + m));
+        } else {
+          const float2 u0 = (hh < K && m < M) ? __ldg(Ab + hh * g.a_ks + m) : make_float2(0.f, 0.f);
+          const float2 u1 = (hh < K && m + 1 < M) ? __ldg(Ab + hh * g.a_ks + m + 1) : make_float2(0.f, 0.f);
+          ra[i][r] = make_float4(u0.x, u0.y, u1.x, u1.y);
+        }
+      }
+    }
+  };
+  auto store_chunk = [&](int st) {
+    uint8_t* sA = stage_base + st * STAGE;
+#pragma unroll
+    for (int i = 0; i < AI; ++i) {
+      const int idx = tid + i * 256;
+      const int mp = idx % (TC_BM / 2), hp = idx / (TC_BM / 2);
+      const float4 v0 = ra[i][0], v1 = ra[i][1];  // (re,im) of m, m+1 at h; at h+1
+      const float4 r0 = make_float4(v0.x, v0.y, v1.x, v1.y), r1 = make_float4(v0.z, v0.w, v1.z, v1.w);
+      const uint32_t o0 = cm_off(2 * mp, 4 * hp, A_LBO), o1 = cm_off(2 * mp + 1, 4 * hp, A_LBO);
+      if (PASSES == 1) {
+        *reinterpret_cast<float4*>(sA + o0) = r0;
+        *reinterpret_cast<float4*>(sA + o1) = r1;
+      } else {
+        const float4 h0 = hi4(r0), h1 = hi4(r1);
+        *reinterpret_cast<float4*>(sA + o0) = h0;
+        *reinterpret_cast<float4*>(sA + o1) = h1;
+        *reinterpret_cast<float4*>(sA + AT + o0) = sub4(r0, h0);
+        *reinterpret_cast<float4*>(sA + AT + o1) = sub4(r1, h1);
+      }
+    }
+  };
+  int64_t gch = 0;
+  int64_t tile = blockIdx.x;
+  if (tile < tiles) load_chunk(tile, 0);
+  for (; tile < tiles; tile += gridDim.x) {
+    const int64_t nb = (tile / mtiles) % nsplit;
+    for (int c = 0; c < nchunks; ++c, ++gch) {
+      const int st = (int)(gch & 1);
+      if (gch >= 2) tc::mbar_wait(&bars[st], (uint32_t)(((gch - 2) >> 1) & 1));  // stage free
+      if (tid == 0)  // W' tile(s) of this chunk straight from the image (L2-resident)
+        bulk_g2s(stage_base + st * STAGE + NPASS * AT, img + (nb * nchunks + c) * (int64_t)(NPASS * BT),
+                 NPASS * BT, &wbars[st]);
+      store_chunk(st);
+      if (c + 1 < nchunks)
+        load_chunk(tile, c + 1);
+      else if (tile + gridDim.x < tiles)
+        load_chunk(tile + gridDim.x, 0);
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::mbar_wait(&wbars[st], (uint32_t)((gch >> 1) & 1));
+        tc::fence_after();
+        const uint32_t a0 = tc::saddr(stage_base + st * STAGE);
+        const uint32_t al = a0 + AT;
+        const uint32_t b0 = a0 + NPASS * AT, bl = b0 + BT;
+#pragma unroll
+        for (int s = 0; s < TC_BK / 8; ++s) {
+          const uint64_t ad = tc::make_desc(a0 + 2 * s * A_LBO, A_LBO, 128);
+          const uint64_t bd = tc::make_desc(b0 + 2 * s * B_LBO, B_LBO, 128);
+          tc::mma_tf32(tmem, ad, bd, IDESC, (c > 0 || s > 0) ? 1u : 0u);
+          if (PASSES > 1) {
+            const uint64_t adl = tc::make_desc(al + 2 * s * A_LBO, A_LBO, 128);
+            const uint64_t bdl = tc::make_desc(bl + 2 * s * B_LBO, B_LBO, 128);
+            tc::mma_tf32(tmem, ad, bdl, IDESC, 1u);
+            tc::mma_tf32(tmem, adl, bd, IDESC, 1u);
+          }
+        }
+        tc::commit(&bars[st]);
+      }
+    }
+    {
+      const int64_t last = gch - 1;
+      tc::mbar_wait(&bars[last & 1], (uint32_t)((last >> 1) & 1));
+      tc::fence_after();
+      const int64_t b = tile / ((int64_t)mtiles * nsplit);
+      const int64_t n0 = nb * (NP / 2);
+      const int lw = warp & 3;  // TMEM lane quarter of this warp
+      const int64_t m = (tile % mtiles) * TC_BM + lw * 32 + lane;
+      float2* Cb = g.C + b * g.c_bs;
+      const int cbeg = (warp >> 2) * (NP / 2), cend = cbeg + NP / 2;
+#pragma unroll 1
+      for (int col = cbeg; col < cend; col += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(lw * 32) << 16) + col, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t n = n0 + col / 2 + q;
+          if (m < M && n < N) Cb[n * g.c_ns + m] = make_float2(g.alpha * v[2 * q], g.alpha * v[2 * q + 1]);
+        }
+      }
+      tc::fence_before();
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
+}
+
 template <int NP, int PASSES>
 __global__ void __launch_bounds__(128, 1) cgemm_tc_kernel(GemmArgs g) {
   using Gm = TcGeo<NP>;
@@ -489,6 +686,46 @@ static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int NP>
+static size_t wimg_bytes_np(int64_t N, int64_t K, int passes) {
+  const int64_t nchunks = (2 * K + TC_BK - 1) / TC_BK, nsplit = (N + NP / 2 - 1) / (NP / 2);
+  return (size_t)(nsplit * nchunks * (passes > 1 ? 2 : 1) * TcGeo<NP>::B_TILE);
+}
+
+size_t cgemm_tc_wimg_bytes(int64_t N, int64_t K, int prec) {
+  if (prec != 1 && prec != 3) return 0;  // TF32 / 3xTF32 only
+  const int passes = prec == 1 ? 1 : 3;
+  const int np = (int)(2 * N);
+  return np <= 64 ? wimg_bytes_np<64>(N, K, passes) : np <= 128 ? wimg_bytes_np<128>(N, K, passes)
+                                                                 : wimg_bytes_np<256>(N, K, passes);
+}
+
+template <int NP, int PASSES>
+static cudaError_t launch_tc_img_t(const GemmArgs& g, cudaStream_t s) {
+  constexpr int STAGE = (PASSES > 1 ? 2 : 1) * (TcGeo<NP>::A_TILE + TcGeo<NP>::B_TILE);
+  const size_t smem = 2 * STAGE + 128;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // 1) W' image
+  {
+    const int64_t nchunks = (2 * g.K + TC_BK - 1) / TC_BK, nsplit = (g.N + NP / 2 - 1) / (NP / 2);
+    const int64_t items = nsplit * nchunks * (NP / 2) * (TC_BK / 4);
+    const int grid = (int)((items + 255) / 256 < 4 * sms ? (items + 255) / 256 : 4 * sms);
+    wimg_kernel<NP, PASSES><<<grid, 256, 0, s>>>(g, reinterpret_cast<uint8_t*>(g.wimg));
+    ++g_launches;
+  }
+  // 2) contraction
+  cudaError_t e =
+      cudaFuncSetAttribute(cgemm_tc_img_kernel<NP, PASSES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * ((g.N + NP / 2 - 1) / (NP / 2)) * g.batch;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  cgemm_tc_img_kernel<NP, PASSES><<<grid, 256, smem, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 bool cgemm_tc_supported(const GemmArgs& g) {
   return g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && g.w_bs == 0 && g.N >= 1;
 }
@@ -500,6 +737,16 @@ cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s) {
     if (np <= 64) return launch_tc_bf16_t<64>(g, s);
     if (np <= 128) return launch_tc_bf16_t<128>(g, s);
     return launch_tc_bf16_t<256>(g, s);
+  }
+  if (g.wimg && (uintptr_t)g.wimg % 16 == 0) {  // W' image in caller scratch
+    if (passes == 1) {
+      if (np <= 64) return launch_tc_img_t<64, 1>(g, s);
+      if (np <= 128) return launch_tc_img_t<128, 1>(g, s);
+      return launch_tc_img_t<256, 1>(g, s);
+    }
+    if (np <= 64) return launch_tc_img_t<64, 3>(g, s);
+    if (np <= 128) return launch_tc_img_t<128, 3>(g, s);
+    return launch_tc_img_t<256, 3>(g, s);
   }
   if (passes == 1) {
     if (np <= 64) return launch_tc_t<64, 1>(g, s);

@@ -517,7 +517,7 @@ static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const
 
 template <class G, int S, int SO>
 static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
-                            const float2* tw, int prec, cudaStream_t st, void (*mark)(cudaStream_t)) {
+                            const float2* tw, int prec, void* wimg, cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
   cudaError_t e = launch_fwd<G, S>(x, A, B * H, tw, false, st);
   if (e != cudaSuccess) return e;
@@ -525,6 +525,7 @@ static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w,
   // channel mixing over modes, 1/(dx*dy) folded into alpha
   const int64_t MQ = (int64_t)G::KX * G::KY;
   GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ, (float)(1.0 / ((double)G::DX * G::NY))};
+  ga.wimg = wimg;
   if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e;
   if (mark) mark(st);
   if ((e = launch_inv<G, SO>(Cm, y, B * N, tw, 1.0f, false, st)) != cudaSuccess) return e;
@@ -570,13 +571,13 @@ cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y
 }
 
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
-                                 float2* Cm, const float2* tw, int prec, cudaStream_t st,
+                                 float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t st,
                                  void (*mark)(cudaStream_t)) {
   const int dx = c->dim_x, kx = c->keep_x;
-  if (dx == 512) return run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, st, mark);
-  if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, st, mark);
-  if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, st, mark);
-  if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, prec, st, mark);
+  if (dx == 512) return run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   return cudaErrorNotSupported;
 }
 

@@ -7,7 +7,7 @@
 namespace tfno {
 bool plane2d_supported(const tfno_cfg* c);
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
-                                 float2* Cm, const float2* tw, int prec, cudaStream_t s,
+                                 float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t s,
                                  void (*mark)(cudaStream_t));
 // natural-order mode tensors [planes][kx][ky] (spectrum API); inverse scaled by `scale`
 cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw, cudaStream_t s);

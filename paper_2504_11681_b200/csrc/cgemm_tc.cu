@@ -270,15 +270,22 @@ __global__ void __launch_bounds__(256, 1) cgemm_tc_img_kernel(GemmArgs g) {
   };
   int64_t gch = 0;
   int64_t tile = blockIdx.x;
-  if (tile < tiles) load_chunk(tile, 0);
+  // W' tile(s) of a chunk straight from the image (L2-resident), one chunk ahead:
+  // chunk j goes to stage j & 1 once the MMAs of chunk j - 2 have drained
+  auto w_issue = [&](int64_t t, int c, int st) {
+    const int64_t nbx = (t / mtiles) % nsplit;
+    bulk_g2s(stage_base + st * STAGE + NPASS * AT, img + (nbx * nchunks + c) * (int64_t)(NPASS * BT), NPASS * BT,
+             &wbars[st]);
+  };
+  if (tile < tiles) {
+    load_chunk(tile, 0);
+    if (tid == 0) w_issue(tile, 0, 0);
+  }
   for (; tile < tiles; tile += gridDim.x) {
     const int64_t nb = (tile / mtiles) % nsplit;
     for (int c = 0; c < nchunks; ++c, ++gch) {
       const int st = (int)(gch & 1);
       if (gch >= 2) tc::mbar_wait(&bars[st], (uint32_t)(((gch - 2) >> 1) & 1));  // stage free
-      if (tid == 0)  // W' tile(s) of this chunk straight from the image (L2-resident)
-        bulk_g2s(stage_base + st * STAGE + NPASS * AT, img + (nb * nchunks + c) * (int64_t)(NPASS * BT),
-                 NPASS * BT, &wbars[st]);
       store_chunk(st);
       if (c + 1 < nchunks)
         load_chunk(tile, c + 1);
@@ -305,6 +312,15 @@ __global__ void __launch_bounds__(256, 1) cgemm_tc_img_kernel(GemmArgs g) {
           }
         }
         tc::commit(&bars[st]);
+        // prefetch the next chunk's W' into the other stage once its MMAs (chunk gch - 1) drained
+        const bool more = c + 1 < nchunks || tile + gridDim.x < tiles;
+        if (more) {
+          if (gch >= 1) tc::mbar_wait(&bars[st ^ 1], (uint32_t)(((gch - 1) >> 1) & 1));
+          if (c + 1 < nchunks)
+            w_issue(tile, c + 1, st ^ 1);
+          else
+            w_issue(tile + gridDim.x, 0, st ^ 1);
+        }
       }
     }
     {

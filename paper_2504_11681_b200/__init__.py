@@ -21,4 +21,6 @@ from .pipeline import (ARRAY_NAMES, MODES, ConfigMismatch, FusedSchedule, Schedu
                        layer_schedule, model_ledger, run_fused, run_layer, run_layer_device, run_staged,
                        traffic_delta, workspace_bytes)
 
+from .autograd import layer_backward, spectral_layer  # noqa: F401,E402  (backward pass, §8f row 4)
+
 __version__ = "0.1.0"

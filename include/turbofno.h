@@ -136,6 +136,13 @@ int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* 
                     int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
                     int64_t c_ns, int64_t c_bs, float alpha, int prec, void* stream);
 
+/* Plane modulation (symmetric +-mode truncation, an extension beyond the reference):
+ * out[p][x][y] = scale * in[p][x][y] * exp(sign * 2*pi*i * (sx*x/dx + sy*y/dy)), sign = +1 / -1.
+ * Modulating by (+keep_x/2, +keep_y/2) before and (-keep_x/2, -keep_y/2) after the first-keep
+ * layer keeps the frequencies [-keep/2, keep/2) on each axis.  in == out is allowed. */
+int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, const void* in, void* out,
+                  float scale, void* stream);
+
 /* Kernels of this library launched by the calling thread since load (library
  * kernels of the staged baseline, cuFFT/cuBLAS, are not counted). */
 long long tfno_launch_count(void);

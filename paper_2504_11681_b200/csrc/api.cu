@@ -543,6 +543,19 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
   return cuda_status(launch_cgemm(g, (cudaStream_t)stream));
 }
 
+int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, const void* in, void* out, float scale,
+                  void* stream) {
+  if (planes < 0 || !pow2(dx) || !pow2(dy) || dx > TFNO_TW_MAX || dy > TFNO_TW_MAX || (sign != 1 && sign != -1))
+    return TFNO_EINVAL;
+  if (planes == 0) return TFNO_OK;
+  if (!in || !out) return TFNO_EINVAL;
+  int err = 0;
+  const float2* tw = twiddle_table(err);
+  if (err) return err;
+  return cuda_status(launch_modulate((const float2*)in, (float2*)out, planes, dx, dy, sx, sy, sign, scale, tw,
+                                     (cudaStream_t)stream));
+}
+
 size_t tfno_spectrum_workspace_bytes(const tfno_cfg* c, int direction) {
   if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
   if (c->rank != 2 || plane2d_supported(c)) return 0;

@@ -662,6 +662,33 @@ cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cuda
 }
 
 // ------------------------------------------------------------------------
+// plane modulation: out = scale * in * w_TW^{-sign*(sx*x*(TW/dx) + sy*y*(TW/dy)) mod TW}
+// (the master table holds exp(-2 pi i k / TW)); float4 = two complex per thread
+__global__ void modulate_kernel(const float2* __restrict__ in, float2* __restrict__ out, int64_t total, int dx,
+                                int dy, int sx, int sy, int sign, float scale, const float2* __restrict__ tw) {
+  const int64_t per = (int64_t)dx * dy;
+  const int ux = TFNO_TW_MAX / dx, uy = TFNO_TW_MAX / dy;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % per);
+    const int xx = r / dy, yy = r % dy;
+    const int k = (int)(((int64_t)sx * xx * ux + (int64_t)sy * yy * uy) & (TFNO_TW_MAX - 1));
+    float2 w = __ldg(&tw[k]);  // exp(-2 pi i k / TW)
+    if (sign > 0) w.y = -w.y;  // exp(+2 pi i k / TW)
+    out[i] = cscale(cmul(__ldg(&in[i]), w), scale);
+  }
+}
+
+cudaError_t launch_modulate(const float2* in, float2* out, int64_t planes, int dx, int dy, int sx, int sy, int sign,
+                            float scale, const float2* tw, cudaStream_t s) {
+  const int64_t total = planes * dx * dy;
+  if (total <= 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  modulate_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, out, total, dx, dy, sx, sy, sign, scale, tw);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // staged baseline copy passes: dst[plane][x][y] = x<cx && y<cy ? scale*src : 0
 // ------------------------------------------------------------------------
 __global__ void pad_truncate_kernel(const float2* __restrict__ src, int64_t planes, int sx, int sy,

@@ -75,6 +75,8 @@ inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s
   return cudaErrorNotSupported;
 }
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
+cudaError_t launch_modulate(const float2* in, float2* out, int64_t planes, int dx, int dy, int sx, int sy, int sign,
+                            float scale, const float2* tw, cudaStream_t s);
 // warp-synchronous register FFT rows (warpfft.cu): n in {256, 1024}, keep / src_len <= n/4
 bool warp_fft_supported(int n, int dir, int keep, int src_len);
 cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2* out, int64_t os, int64_t P,

@@ -366,8 +366,9 @@ template <int U>
 struct TfGeo {
   static constexpr int T = 32 * U, N = 32 * T, NTH = 512, TEAMS = NTH / T;
   static constexpr int LU = U == 4 ? 2 : 1;
-  static constexpr size_t smem_bytes() {
-    return sizeof(float2) * ((size_t)32 + (size_t)32 * T + (size_t)TEAMS * T * 32 + (size_t)T);
+  __host__ __device__ static constexpr size_t smem_bytes(int k2 = 0) {  // + inverse mode-row buffers (TEAMS x 2 x 32*K2)
+    return sizeof(float2) * ((size_t)32 + (size_t)32 * T + (size_t)TEAMS * T * 32 + (size_t)T +
+                             (size_t)TEAMS * 2 * 32 * k2);
   }
   // [t][k1] tile (row length 32, unpadded) with the column XOR-swizzled by a
   // 4-bit rotation of t: conflict-free both for 16 consecutive t at fixed k1
@@ -464,18 +465,49 @@ __global__ void __launch_bounds__(512, 1) team_fft_inv_kernel(const float2* __re
   }
   __syncthreads();
   float2* trr = tr + team * T * 32;
+  // cp.async double buffer of the mode rows when it fits in shared memory (PF)
+  constexpr bool PF = G::smem_bytes(K2) <= 227 * 1024;
+  float2* mbuf = twT + T + team * 2 * (32 * K2);  // this team's double-buffered mode rows
   const int k1s = tt / U, us = tt % U;
-  for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS) {
+  // next row's nonzero modes: cp.async global -> shared one row ahead (the
+  // per-row __ldg of the modes was the exposed latency: long-scoreboard stalls)
+  const bool vec = (in_stride % 2 == 0) && (((uintptr_t)in & 15) == 0);
+  auto prefetch = [&](int64_t r, int buf) {
+    if constexpr (!PF) return;
+    float2* d = mbuf + buf * (32 * K2);
+    const float2* sr = in + r * in_stride;
+    if (vec) {
+      for (int e = 2 * tt; e < 32 * K2; e += 2 * T) {
+        const int nb = e + 1 < src_len ? 16 : (e < src_len ? 8 : 0);
+        const unsigned sd = (unsigned)__cvta_generic_to_shared(d + e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sd), "l"(nb ? sr + e : sr), "r"(nb)
+                     : "memory");
+      }
+    } else {
+      for (int e = tt; e < 32 * K2; e += T) d[e] = e < src_len ? __ldg(&sr[e]) : make_float2(0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int it = 0;
+  if (PF && (int64_t)blockIdx.x * G::TEAMS + team < P) prefetch((int64_t)blockIdx.x * G::TEAMS + team, 0);
+  for (int64_t row0 = (int64_t)blockIdx.x * G::TEAMS; row0 < P; row0 += (int64_t)gridDim.x * G::TEAMS, ++it) {
     const int64_t row = row0 + team;
     const bool live = row < P;
-    const float2* src = in + (live ? row : 0) * in_stride;
+    const int64_t nrow = row + (int64_t)gridDim.x * G::TEAMS;
+    if constexpr (PF) {
+      if (nrow < P) prefetch(nrow, (it + 1) & 1);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this row's pieces landed
+      named_bar_sync(1 + team, T);                           // ... everyone's
+    }
+    const float2* src = PF ? mbuf + (it & 1) * (32 * K2) : in + (live ? row : 0) * in_stride;
     // thread (k1s, us): inputs X[k1s + 32 k2] w_T^{+k2 us}, padded DFT32 over k2 -> s
     float2 z[32];
 #pragma unroll
     for (int k2 = 0; k2 < 32; ++k2) {
       if (k2 < K2) {
         const int k = k1s + 32 * k2;
-        float2 xv = (live && k < src_len) ? __ldg(&src[k]) : make_float2(0.f, 0.f);
+        float2 xv = (live && k < src_len) ? src[k] : make_float2(0.f, 0.f);
         z[k2] = (us && k2) ? cmul(xv, conjf2(twT[(us * k2) % T])) : xv;
       } else {
         z[k2] = make_float2(0.f, 0.f);
@@ -518,9 +550,10 @@ static cudaError_t launch_tf(int dir, const float2* in, int64_t is, float2* out,
     if (e != cudaSuccess) return e;
     team_fft_fwd_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw);
   } else {
-    e = cudaFuncSetAttribute(team_fft_inv_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem_i = G::smem_bytes(K2) <= 227 * 1024 ? G::smem_bytes(K2) : smem;
+    e = cudaFuncSetAttribute(team_fft_inv_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i);
     if (e != cudaSuccess) return e;
-    team_fft_inv_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, src_len, scale, tw);
+    team_fft_inv_kernel<U, K2><<<grid, G::NTH, smem_i, s>>>(in, is, out, os, P, src_len, scale, tw);
   }
   ++g_launches;
   return cudaGetLastError();

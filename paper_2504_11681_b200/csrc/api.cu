@@ -150,7 +150,7 @@ cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st
 // schedule decision shared by workspace sizing and the forward
 struct Sched {
   bool staged = false, plane2d = false, rows_fast = false, warp_fused = false, f1 = false;
-  int rows_NT = 0, f1_split = 1;
+  int rows_NT = 0, f1_split = 1, f1_cluster = 1;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
   int launches = 0;
@@ -199,7 +199,8 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
   if (mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy &&
       fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
     s.f1 = true;
-    s.f1_split = fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
+    s.f1_cluster = fused1d_cluster((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
+    s.f1_split = s.f1_cluster > 1 ? 1 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
     s.fg = s.gi = true;
     s.need_s1 = s.need_mid = (g.rank == 2);
     s.launches = (g.rank == 2) ? 3 : 1;
@@ -684,6 +685,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
       fa.N = (int)g.N;
       fa.NT = (s.warp_fused || s.f1) ? (int)g.N : s.rows_NT;
       fa.nsplit = s.f1 ? s.f1_split : 1;
+      fa.cluster = s.f1 ? s.f1_cluster : 1;
       fa.KC = rows_chunk((int)g.dy);
       fa.EC = fa.KC;
     } else {

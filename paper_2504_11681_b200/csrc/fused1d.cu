@@ -72,13 +72,49 @@ template <int L>
 __device__ __forceinline__ int tsw(int r, int c) {
   return r * L + (c ^ r);
 }
+// ---- cluster / DSMEM helpers (hidden-channel split over a thread-block cluster)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float2 ld_dsmem(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(10000000u)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // 8 x 16 tile of the N = 128 rows ([k1][t]): the column is XOR-ed with 2*k1 so
 // the row writes (16 consecutive t) and the (k1 = lane/2, t = lane%2 + 2t')
 // reads of a half warp are both conflict free.
 __device__ __forceinline__ int tsw8(int r, int c) { return r * 16 + (c ^ (2 * r)); }
 
-template <int L, int V, int KP, int TI, int TJ, int NOUT>
+template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS>
 __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
+  // CS > 1: a cluster of CS CTAs shares each item: CTA r transforms and mixes
+  // the hidden channels [r*H/CS, (r+1)*H/CS), the CS partial C tiles are summed
+  // in a fixed order over distributed shared memory, and CTA r runs the
+  // inverse of output rows [r*NOUT/CS, (r+1)*NOUT/CS).
   using G = F1Geo<L, V, KP, TI, TJ, NOUT>;
   constexpr int N = G::N, TEAMS = G::TEAMS, KC = G::KC, KT = G::KT, MT = G::MT, NTG = G::NTG, NA = G::NA;
   constexpr int NGW = G::NGT / 32, NS = G::NSLOT;
@@ -102,9 +138,13 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 
   const int tid = threadIdx.x;
   const int keep = a.keep;
-  const int nchunks = a.H / KC;
-  const int S = a.nsplit > 1 ? a.nsplit : 1;  // items = row groups x output-channel splits
+  const int cr = CS > 1 ? (int)cluster_rank() : 0;
+  const int Hc = a.H / CS, h_off = cr * Hc;  // this CTA's hidden channels
+  const int nchunks = Hc / KC;
+  const int S = (CS == 1 && a.nsplit > 1) ? a.nsplit : 1;  // items = row groups x output-channel splits
   const int64_t items = a.G * S;
+  const int64_t first = CS > 1 ? (int64_t)(blockIdx.x / CS) : (int64_t)blockIdx.x;  // item stride: units
+  const int64_t units = CS > 1 ? (int64_t)(gridDim.x / CS) : (int64_t)gridDim.x;
   for (int k = tid; k < L; k += blockDim.x) twL[k] = __ldg(&a.twg[(size_t)k * (TFNO_TW_MAX / L)]);
   for (int i = tid; i < N; i += blockDim.x) {  // [k1][t] = w_N^{t k1}, k1 < V, t < L
     const int k1 = i / L, t = i % L;
@@ -123,23 +163,24 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
       mbar_init(&afull[s], TEAMS);
       mbar_init(&aempty[s], NGW);
     }
-    mbar_init(cfull, NGW);
-    mbar_init(cempty, TEAMS);
+    mbar_init(cfull, CS * NGW);    // every CTA of the cluster publishes its partial C
+    mbar_init(cempty, CS * TEAMS); // every CTA of the cluster has read this CTA's partial
     fence_mbar_init();
   }
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
 
   if (tid >= G::NFT + G::NGT) {
     // ================= producer warpgroup (one elected thread issues)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_PROD));
     if (tid == G::NFT + G::NGT) {
-      const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      const int64_t nmine = (items - first + units - 1) / units;
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_w = policy_evict_last();
       const uint32_t wbytes = (uint32_t)(KC * NOUT * sizeof(float2));
       int64_t kk = 0;  // chunks issued so far (the same count for every team)
       for (int64_t it = 0; it < nmine; ++it) {
-        const int64_t item = blockIdx.x + it * gridDim.x;
+        const int64_t item = first + it * units;
         const int64_t g = item / S, n0 = (item % S) * NOUT;
         const int64_t bb = g / a.gx, pp = g % a.gx;
         const float2* xg = a.x + bb * a.x_sb + pp * a.x_sp;
@@ -151,13 +192,14 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
             const int b = t * NS + rs;
             if (use >= 1) mbar_wait(&empty[b], (uint32_t)((use - 1) & 1));
             mbar_expect_tx(&full[b], N * sizeof(float2));
-            tma_load_1d(slots + b * N, xg + (int64_t)(c * KC + t) * a.x_sh, N * sizeof(float2), &full[b], pol_x);
+            tma_load_1d(slots + b * N, xg + (int64_t)(h_off + c * KC + t) * a.x_sh, N * sizeof(float2), &full[b],
+                        pol_x);
           }
           const int ws = (int)(kk & 1);
           if (kk >= 2) mbar_wait(&wempty[ws], (uint32_t)(((kk >> 1) - 1) & 1));
           mbar_expect_tx(&wfull[ws], wbytes);
           if (S == 1) {
-            tma_load_1d(Wr + ws * KC * NOUT, a.W + (int64_t)c * KC * NOUT, wbytes, &wfull[ws], pol_w);
+            tma_load_1d(Wr + ws * KC * NOUT, a.W + (int64_t)(h_off + c * KC) * NOUT, wbytes, &wfull[ws], pol_w);
           } else {  // this split's columns W[h][n0:n0+NOUT], one bulk copy per row
 #pragma unroll 1
             for (int r = 0; r < KC; ++r)
@@ -173,7 +215,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   if (tid >= G::NFT) {
     // ================= GEMM warps
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_GEMM));
-    const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nmine = (items - first + units - 1) / units;
     const int gt = tid - G::NFT;
     const int tm = gt % MT, tn = gt / MT;
     int64_t kk = 0;
@@ -208,20 +250,32 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         }
       }
       // hand the C tile to the FFT warps (once they are done with the previous one)
-      if (it >= 1) mbar_wait(cempty, (uint32_t)((it - 1) & 1));
+      if (it >= 1) {
+        if constexpr (CS > 1)
+          mbar_wait_cluster(cempty, (uint32_t)((it - 1) & 1));
+        else
+          mbar_wait(cempty, (uint32_t)((it - 1) & 1));
+      }
 #pragma unroll
       for (int j = 0; j < TJ; ++j)
 #pragma unroll
         for (int i = 0; i < TI; ++i) Cs[(tn + NTG * j) * KT + tm + MT * i] = acc[i][j];
-      __syncwarp();
-      if ((gt & 31) == 0) mbar_arrive(cfull);
+      if constexpr (CS > 1) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        __syncwarp();
+        if ((gt & 31) == 0)
+          for (int r = 0; r < CS; ++r) mbar_arrive_cluster(mapa_rank(cfull, (uint32_t)r));
+      } else {
+        __syncwarp();
+        if ((gt & 31) == 0) mbar_arrive(cfull);
+      }
     }
     return;
   }
 
   // ================= FFT warps
   if constexpr (G::REG_FFT > G::REG_LAUNCH) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
-  const int64_t nmine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;  // grid <= items
+  const int64_t nmine = (items - first + units - 1) / units;  // grid <= items
   const int lane = tid % L, team = tid / L;
   const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));
   float2* trr = tr + team * N;
@@ -303,19 +357,34 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
     }
     if (it >= 1) {
       // ---- zero-padded inverse of item it-1's output rows from the C tile
-      const int64_t item = blockIdx.x + (it - 1) * gridDim.x;
+      const int64_t item = first + (it - 1) * units;
       const int64_t g = item / S, n0 = (item % S) * NOUT;
       const int64_t bb = g / a.gx, pp = g % a.gx;
       float2* yg = a.y + bb * a.y_sb + pp * a.y_sp + n0 * a.y_sn;
-      mbar_wait(cfull, (uint32_t)((it - 1) & 1));
-      for (int n = team; n < NOUT; n += TEAMS) {
+      constexpr int NC = NOUT / CS;  // output rows of this CTA: [cr*NC, (cr+1)*NC)
+      if constexpr (CS > 1)
+        mbar_wait_cluster(cfull, (uint32_t)((it - 1) & 1));
+      else
+        mbar_wait(cfull, (uint32_t)((it - 1) & 1));
+      // C[n][q]: own tile, or the fixed-order sum of the cluster's partial tiles (DSMEM)
+      auto cval = [&](int n, int q) -> float2 {
+        if constexpr (CS == 1) {
+          return Cs[n * KT + q];
+        } else {
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int r = 0; r < CS; ++r) s2 = cadd(s2, ld_dsmem(mapa_rank(Cs + n * KT + q, (uint32_t)r)));
+          return s2;
+        }
+      };
+      for (int n = cr * NC + team; n < (cr + 1) * NC; n += TEAMS) {
         float2* dst = yg + (int64_t)n * a.y_sn;
         if constexpr (V == L) {
         float2 xk[KP];
 #pragma unroll
         for (int k2 = 0; k2 < KP; ++k2) {
           const int q = lane + L * k2;
-          xk[k2] = q < keep ? Cs[n * KT + q] : make_float2(0.f, 0.f);
+          xk[k2] = q < keep ? cval(n, q) : make_float2(0.f, 0.f);
         }
         float2 z[L];
         wf::idftL_padded<L, KP>(xk, z, twL);
@@ -340,7 +409,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
           const int q = k1 + 8 * k2;
-          z[k2] = (k2 < K2 && q < keep) ? Cs[n * KT + q] : make_float2(0.f, 0.f);
+          z[k2] = (k2 < K2 && q < keep) ? cval(n, q) : make_float2(0.f, 0.f);
           if (k2 < K2 && k2 && hf) z[k2] = cmul(z[k2], conjf2(twL[k2]));
         }
         dft8<1>(z);
@@ -359,9 +428,18 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         }
       }
       __syncwarp(tmask);
-      if (lane == 0) mbar_arrive(cempty);
+      if (lane == 0) {
+        if constexpr (CS > 1) {
+          for (int r = 0; r < CS; ++r) mbar_arrive_cluster(mapa_rank(cempty, (uint32_t)r));
+        } else {
+          mbar_arrive(cempty);
+        }
+      }
     }
   }
+  // peers read this CTA's last partial tile over DSMEM: stay resident until they are done
+  if constexpr (CS > 1)
+    if (nmine > 0) mbar_wait_cluster(cempty, (uint32_t)((nmine - 1) & 1));
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -391,23 +469,42 @@ static const F1Shape* f1_pick(int n, int keep, int H, int NO) {
 
 bool fused1d_supported(int n, int keep, int H, int NO) { return f1_pick(n, keep, H, NO) != nullptr; }
 
-template <int L, int V, int KP, int TI, int TJ, int NOUT>
+template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS>
 static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
   using G = F1Geo<L, V, KP, TI, TJ, NOUT>;
   static_assert(G::smem_bytes() <= 227 * 1024, "shared memory");
   const size_t smem = G::smem_bytes();
   if ((uintptr_t)a.x % 16 || (uintptr_t)a.W % 16 || (a.x_sh % 2) || (a.x_sb % 2) || (a.x_sp % 2))
     return cudaErrorNotSupported;  // TMA bulk copies need 16-byte aligned rows
-  cudaError_t e = cudaFuncSetAttribute(fused1d_kernel<L, V, KP, TI, TJ, NOUT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = fused1d_kernel<L, V, KP, TI, TJ, NOUT, CS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t items = a.G * (a.nsplit > 1 ? a.nsplit : 1);
-  const int grid = (int)(items < sms ? items : sms);
-  if (grid < 1) return cudaSuccess;
-  fused1d_kernel<L, V, KP, TI, TJ, NOUT><<<grid, G::NTH, smem, s>>>(a);
+  if (CS == 1) {
+    const int64_t items = a.G * (a.nsplit > 1 ? a.nsplit : 1);
+    const int grid = (int)(items < sms ? items : sms);
+    if (grid < 1) return cudaSuccess;
+    kern<<<grid, G::NTH, smem, s>>>(a);
+  } else {
+    const int64_t units = a.G < sms / CS ? a.G : sms / CS;
+    if (units < 1) return cudaSuccess;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(units * CS));
+    cfg.blockDim = dim3(G::NTH);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaSuccess) return e;
+  }
   ++g_launches;
   return cudaGetLastError();
 }
@@ -422,13 +519,34 @@ int fused1d_split(int n, int keep, int H, int NO, int64_t G) {
   return S;
 }
 
+int fused1d_cluster(int n, int keep, int H, int NO, int64_t G) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TFNO_FUSED1D_CLUSTER");
+    env = e ? atoi(e) : -1;
+  }
+  if (env == 0 || !f1_pick(n, keep, H, NO)) return 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int L = (n == 256 || n == 128) ? 16 : 32, KC = 256 / L;
+  int CS = 1;  // split the hidden channels while the clusters still fit one wave of SMs
+  while (CS < 4 && G * 2 * CS <= sms && H % (2 * CS * KC) == 0 && NO % (2 * CS) == 0) CS *= 2;
+  return CS;
+}
+
 cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s) {
-  const int S = a.nsplit > 1 ? a.nsplit : 1;
+  const int CS = a.cluster > 1 ? a.cluster : 1;
+  const int S = (CS == 1 && a.nsplit > 1) ? a.nsplit : 1;
   if (a.N % S) return cudaErrorNotSupported;
   const F1Shape* p = f1_pick(a.n, a.keep, a.H, a.N / S);
   if (!p) return cudaErrorNotSupported;
-#define F1_CASE(LL, VV, KK, TI_, TJ_, NO_) \
-  if (p->L == LL && p->V == VV && p->KP == KK && p->NOUT == NO_) return launch_f1<LL, VV, KK, TI_, TJ_, NO_>(a, s);
+#define F1_CASE(LL, VV, KK, TI_, TJ_, NO_)                                                          \
+  if (p->L == LL && p->V == VV && p->KP == KK && p->NOUT == NO_) {                                  \
+    if (CS == 4) return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 4>(a, s);                             \
+    if (CS == 2) return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 2>(a, s);                             \
+    return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 1>(a, s);                                          \
+  }
   F1_CASE(16, 16, 1, 1, 4, 64) F1_CASE(16, 16, 1, 1, 8, 128) F1_CASE(16, 16, 1, 2, 8, 256)
   F1_CASE(16, 16, 2, 1, 4, 32)
   F1_CASE(16, 16, 2, 2, 4, 64) F1_CASE(16, 16, 2, 2, 8, 128) F1_CASE(16, 16, 2, 4, 8, 256)

@@ -52,6 +52,7 @@ struct FusedArgs {
   int64_t c_sb, c_sp, c_sn;  // C row (g,n), contiguous keep
   int NT, KC, EC;
   int nsplit;  // fused1d: output channels split over nsplit CTAs per row group (forward recomputed)
+  int cluster;  // fused1d: hidden channels split over a cluster of CTAs, partial C reduced over DSMEM
   const float2* twg;
   float inv_scale;
 };
@@ -87,6 +88,8 @@ bool warp_fused_supported(int n, int keep, int H, int NO);
 bool fused1d_supported(int n, int keep, int H, int NO);
 // output-channel split for fused1d so that small batches still fill the SMs (0 = unsupported)
 int fused1d_split(int n, int keep, int H, int NO, int64_t G);
+// hidden-channel cluster split for fused1d (0/1 = none); takes precedence over the output split
+int fused1d_cluster(int n, int keep, int H, int NO, int64_t G);
 cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_warp_fused(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int sy, int64_t s_plane,

@@ -61,7 +61,8 @@ struct F1Geo {
   static constexpr size_t smem_bytes() { return BAR_BYTES + sizeof(float2) * (size_t)TOTAL; }
   // register split (setmaxnreg) inside the CTA's launch allocation of 640 x 96:
   // producer warpgroup 24, FFT warps 96 (unchanged), GEMM warps 128
-  static constexpr int REG_LAUNCH = 96, REG_PROD = 24, REG_FFT = 96, REG_GEMM = 128;
+  // (L = 32 rows hold 32 complex values per lane: FFT warps get 112, GEMM warps 112)
+  static constexpr int REG_LAUNCH = 96, REG_PROD = 24, REG_FFT = L == 32 ? 112 : 96, REG_GEMM = L == 32 ? 112 : 128;
   static_assert(128 * REG_PROD + NFT * REG_FFT + NGT * REG_GEMM <= NTH * REG_LAUNCH, "register pool");
 };
 

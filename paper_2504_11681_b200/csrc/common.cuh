@@ -14,24 +14,104 @@
 
 namespace tfno {
 
+// ---- complex arithmetic --------------------------------------------------
+// Blackwell issues packed FP32 (FADD2 / FMUL2 / FFMA2 on a register pair, with
+// broadcast (.F32), swap (.LO_HI) and negation operand modifiers).  A packed
+// instruction takes two FP32-pipe cycles but ONE issue slot, and the FFT /
+// CGEMM kernels here are issue-bound (ncu: ~60% issue, 66% FP instructions),
+// so the complex primitives are written on f32x2 (tools/probes/ffma2_probe.cu
+// measured FFMA2 at the FFMA FLOP rate).  -DTFNO_SCALAR_COMPLEX restores the
+// scalar forms for A/B.  Results are IEEE FP32 either way; only the operation
+// grouping inside cmul/cmac differs (which product is rounded before the FMA).
+#ifndef TFNO_SCALAR_COMPLEX
+typedef unsigned long long tfno_pair;
+__device__ __forceinline__ tfno_pair pk2(float2 v) {
+  tfno_pair r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(tfno_pair v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  tfno_pair r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  tfno_pair r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  tfno_pair r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  tfno_pair r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return sub2(a, b); }
+// a * b: (a.x, a.x) * (b.x, b.y) + (a.y, a.y) * (-b.y, b.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return fma2(make_float2(a.y, a.y), make_float2(-b.y, b.x), mul2(make_float2(a.x, a.x), b));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return mul2(a, make_float2(s, s)); }
+// acc += a * b (2 FFMA2 + the (-b.y, b.x) companion, shared across uses of b)
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
+  acc = fma2(make_float2(a.x, a.x), b, acc);
+  acc = fma2(make_float2(a.y, a.y), make_float2(-b.y, b.x), acc);
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
-// multiply by -i (forward, DIR = -1) or +i (inverse, DIR = +1)
-template <int DIR>
-__device__ __forceinline__ float2 mul_dir_i(float2 a) {
-  return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
-}
 // acc += a * b (4 FFMA)
 __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
   acc.x = fmaf(a.x, b.x, acc.x);
   acc.x = fmaf(-a.y, b.y, acc.x);
   acc.y = fmaf(a.x, b.y, acc.y);
   acc.y = fmaf(a.y, b.x, acc.y);
+}
+#endif
+// scalar 4-FFMA complex MAC: the SIMT mode CGEMMs are FMA-pipe-bound, where the
+// packed form measured slower (C4 contraction 1.46 -> 1.54 ms)
+__device__ __forceinline__ void cmac_s(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+// multiply by -i (forward, DIR = -1) or +i (inverse, DIR = +1)
+template <int DIR>
+__device__ __forceinline__ float2 mul_dir_i(float2 a) {
+  return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+// x +/- (DIR i) y: one packed FMA with the swapped y and a (+1, -1) sign pair
+template <int DIR>
+__device__ __forceinline__ float2 cadd_dir_i(float2 x, float2 y) {
+#ifndef TFNO_SCALAR_COMPLEX
+  return fma2(make_float2(y.y, y.x), DIR < 0 ? make_float2(1.f, -1.f) : make_float2(-1.f, 1.f), x);
+#else
+  return cadd(x, mul_dir_i<DIR>(y));
+#endif
+}
+template <int DIR>
+__device__ __forceinline__ float2 csub_dir_i(float2 x, float2 y) {
+#ifndef TFNO_SCALAR_COMPLEX
+  return fma2(make_float2(y.y, y.x), DIR < 0 ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f), x);
+#else
+  return csub(x, mul_dir_i<DIR>(y));
+#endif
 }
 
 // twiddle omega_n^k for direction DIR from the forward table of length n
@@ -49,12 +129,12 @@ __device__ __forceinline__ void dft2(float2& a, float2& b) {
 
 template <int DIR>
 __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
-  float2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
-  float2 t2 = cadd(x1, x3), t3 = mul_dir_i<DIR>(csub(x1, x3));
+  const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
+  const float2 t2 = cadd(x1, x3), d = csub(x1, x3);
   x0 = cadd(t0, t2);
   x2 = csub(t0, t2);
-  x1 = cadd(t1, t3);
-  x3 = csub(t1, t3);
+  x1 = cadd_dir_i<DIR>(t1, d);  // t1 + (DIR i) d
+  x3 = csub_dir_i<DIR>(t1, d);
 }
 
 template <int DIR>
@@ -64,22 +144,15 @@ __device__ __forceinline__ void dft8(float2* v) {
   float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
   dft4<DIR>(e0, e1, e2, e3);
   dft4<DIR>(o0, o1, o2, o3);
-  // o1 *= w8^1, o2 *= w8^2, o3 *= w8^3   (w8 = exp(DIR*2*pi*i/8))
-  float2 t1, t3;
-  if (DIR < 0) {
-    t1 = make_float2((o1.x + o1.y) * r, (o1.y - o1.x) * r);
-    t3 = make_float2((o3.y - o3.x) * r, -(o3.x + o3.y) * r);
-  } else {
-    t1 = make_float2((o1.x - o1.y) * r, (o1.x + o1.y) * r);
-    t3 = make_float2(-(o3.x + o3.y) * r, (o3.x - o3.y) * r);
-  }
-  float2 t2 = mul_dir_i<DIR>(o2);
+  // o1 *= w8^1 = (1 + DIR i)/sqrt2, o3 *= w8^3 = (-1 + DIR i)/sqrt2, o2 *= w8^2 = DIR i
+  const float2 t1 = cscale(cadd_dir_i<DIR>(o1, o1), r);
+  const float2 t3 = cscale(csub(mul_dir_i<DIR>(o3), o3), r);
   v[0] = cadd(e0, o0);
   v[4] = csub(e0, o0);
   v[1] = cadd(e1, t1);
   v[5] = csub(e1, t1);
-  v[2] = cadd(e2, t2);
-  v[6] = csub(e2, t2);
+  v[2] = cadd_dir_i<DIR>(e2, o2);
+  v[6] = csub_dir_i<DIR>(e2, o2);
   v[3] = cadd(e3, t3);
   v[7] = csub(e3, t3);
 }

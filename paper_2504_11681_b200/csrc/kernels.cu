@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cmac(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < 4; ++j) cmac_s(acc[i][j], av[i], bv[j]);
     }
     __syncthreads();
   }
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
 #pragma unroll
       for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < TJ; ++j) cmac_s(acc[i][j], av[i], bv[j]);
     }
     if (more) {
       store_chunk(buf ^ 1);

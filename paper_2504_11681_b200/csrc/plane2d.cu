@@ -464,7 +464,7 @@ constexpr size_t inv_smem(int SO, bool dst = false) {
 // (profiles/r01/plane_variants.txt); TFNO_PLANE_VARIANT overrides for A/B runs.
 template <class G>
 constexpr int plane_variant_default() {
-  return G::DX == 512 ? 0 : (G::KX == 16 && G::DX == 256) ? 3 : 1;
+  return (G::KX == 16 && G::DX == 256) ? 3 : 1;  // re-measured with packed f32x2 math (profiles/r01/plane_variants.txt)
 }
 template <class G>
 static int plane_variant() {

@@ -36,18 +36,20 @@
 namespace tfno {
 
 // ---------------------------------------------------------------- geometry
-template <int DX_, int KX_, int NY_, int KY_, int NTH_>
+template <int DX_, int KX_, int NY_, int KY_, int NTH_, int RPT_ = 1>
 struct PlaneGeo {
   static constexpr int DX = DX_, KX = KX_, NY = NY_, KY = KY_, NTH = NTH_;
+  static constexpr int RPT = RPT_;  // rows per thread team per iteration (forward ILP)
   static constexpr int M = NY / 8;  // threads per row team
   static constexpr int A = M / 8;
   static constexpr int T = (KY + 7) / 8;
   static constexpr int LOGA = (A >= 16 ? 4 : A >= 8 ? 3 : A >= 4 ? 2 : A >= 2 ? 1 : 0);
   static constexpr int LOGT = (T >= 8 ? 3 : T >= 4 ? 2 : T >= 2 ? 1 : 0);
-  static constexpr int TEAMS = NTH / M;  // rows per iteration
+  static constexpr int TEAMS = NTH / M;  // thread teams
+  static constexpr int ROWS = TEAMS * RPT;  // rows per iteration
   static constexpr int R = DX / KX;      // four-step classes along x
   static constexpr int KA = KX / 8;      // kx = 8 * KA
-  static constexpr int IPC = KX / TEAMS; // iterations per class
+  static constexpr int IPC = KX / ROWS;  // iterations per class
   static constexpr int PAD = ((-7 * A) % 16 + 16) % 16;
   static constexpr int RT = T + 2;                 // reduction buffer: padded t-stride
   static constexpr int RS = A * RT + 8;            //                   per-r stride
@@ -56,7 +58,7 @@ struct PlaneGeo {
   static_assert(A >= 1 && (1 << LOGA) == A, "A power of two");
   static_assert((1 << LOGT) == T && T <= A && T <= 8, "ky <= 8*min(8, dy/64)");
   static_assert(8 * T == KY, "ky multiple of 8");
-  static_assert(KX % 8 == 0 && KA <= 8 && KX % TEAMS == 0 && DX % KX == 0, "kx shape");
+  static_assert(KX % 8 == 0 && KA <= 8 && KX % ROWS == 0 && DX % KX == 0, "kx shape");
   static_assert(NTH % M == 0 && (M % 32 == 0 || 32 % M == 0), "team shape");
 };
 
@@ -85,12 +87,13 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
                        const float2* __restrict__ twg) {
   constexpr int NY = G::NY, M = G::M, A = G::A, T = G::T, TEAMS = G::TEAMS, R = G::R, KA = G::KA;
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
-  constexpr int RT = G::RT, RS = G::RS;
+  constexpr int RT = G::RT, RS = G::RS, RPT = G::RPT, ROWS = G::ROWS;
+  static_assert(RPT == 1 || !DLD, "direct loads only with one row per team");
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);
-  float2* tr = ring + (DLD ? 0 : S * TEAMS * NY);  // DLD: rows go straight to registers (no ring)
-  float2* red = tr + TEAMS * 8 * TS;
-  float2* Tc = red + TEAMS * 8 * RS;
+  float2* tr = ring + (DLD ? 0 : S * ROWS * NY);  // DLD: rows go straight to registers (no ring)
+  float2* red = tr + ROWS * 8 * TS;
+  float2* Tc = red + ROWS * 8 * RS;
   float2* twy = Tc + KX * KY;
   float2* twx = twy + NY;
   uint64_t* full = reinterpret_cast<uint64_t*>(twx + DX);
@@ -124,11 +127,11 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
         for (int x0 = 0; x0 < R; ++x0) {
           for (int j = 0; j < IPC; ++j, ++cnt) {
             if (cnt >= S) mbar_wait(&empty[slot], phase ^ 1u);
-            float2* dst = ring + slot * TEAMS * NY;
-            mbar_expect_tx(&full[slot], TEAMS * NY * 8);
+            float2* dst = ring + slot * ROWS * NY;
+            mbar_expect_tx(&full[slot], ROWS * NY * 8);
 #pragma unroll 1
-            for (int tm = 0; tm < TEAMS; ++tm) {
-              const int row = x0 + R * (j * TEAMS + tm);
+            for (int tm = 0; tm < ROWS; ++tm) {
+              const int row = x0 + R * (j * ROWS + tm);
               tma_load_1d(dst + tm * NY, src + (int64_t)row * NY, NY * 8, &full[slot], pol);
             }
             if (++slot == S) {
@@ -145,8 +148,9 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   // ---------------- compute threads
   const int team = tid / M, tt = tid % M;
   const int a_ = tt % A, r_ = tt / A;
-  float2* trt = tr + team * 8 * TS;
-  float2* redt = red + team * 8 * RS;
+  // row tm = team + TEAMS * r2 of the iteration (r2 < RPT): its transpose / reduction buffers
+  auto trt = [&](int r2) { return tr + (team + TEAMS * r2) * 8 * TS; };
+  auto redt = [&](int r2) { return red + (team + TEAMS * r2) * 8 * RS; };
   // per-thread constant twiddles (a strided table walk is an 8-way bank conflict)
   float2 tw1[8], tw2[8];
 #pragma unroll
@@ -190,66 +194,88 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   for (int j = 0; j < IPC; ++j, ++it) {
     if (!DLD) mbar_wait(&full[slot], phase);
     // ---- row stage 1: radix-8 over y2, twiddle w_N^{r*y1}, transpose
+    // (RPT independent rows per thread, interleaved for ILP)
     {
-      float2 v[8];
+      float2 v[RPT][8];
       if (DLD) {
 #pragma unroll
-        for (int y2 = 0; y2 < 8; ++y2) v[y2] = nxt[y2];
+        for (int y2 = 0; y2 < 8; ++y2) v[0][y2] = nxt[y2];
         if (it + 1 < NIT) {
           const float2* rp = row_ptr((int64_t)it + 1);
 #pragma unroll
           for (int y2 = 0; y2 < 8; ++y2) nxt[y2] = __ldcs(rp + tt + M * y2);
         }
       } else {
-        const float2* row = ring + slot * TEAMS * NY + team * NY;
 #pragma unroll
-        for (int y2 = 0; y2 < 8; ++y2) v[y2] = row[tt + M * y2];
+        for (int r2 = 0; r2 < RPT; ++r2) {
+          const float2* row = ring + slot * ROWS * NY + (team + TEAMS * r2) * NY;
+#pragma unroll
+          for (int y2 = 0; y2 < 8; ++y2) v[r2][y2] = row[tt + M * y2];
+        }
       }
-      dft8<-1>(v);
+#pragma unroll
+      for (int r2 = 0; r2 < RPT; ++r2) dft8<-1>(v[r2]);
       if (!DLD) {
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
       }
 #pragma unroll
-      for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
+      for (int r2 = 0; r2 < RPT; ++r2) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) trt[r * TS + tt] = v[r];
+        for (int r = 1; r < 8; ++r) v[r2][r] = cmul(v[r2][r], tw1[r]);
+        float2* tb = trt(r2);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) tb[r * TS + tt] = v[r2][r];
+      }
     }
     team_sync<M>(team);
     // ---- row stage 2: radix-8 over c, twiddle w_M^{t*a} -> reduction buffer
     {
-      float2 u[8];
+      float2 u[RPT][8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) u[c] = trt[r_ * TS + a_ + A * c];
-      dft8<-1>(u);  // twiddle w_M^{t a} deferred to the reduction (FMA-fused)
-      float2* dst = redt + r_ * RS + a_ * RT;
-      if constexpr (T % 2 == 0) {
+      for (int r2 = 0; r2 < RPT; ++r2) {
+        const float2* tb = trt(r2);
 #pragma unroll
-        for (int t = 0; t < T; t += 2)
-          *reinterpret_cast<float4*>(dst + t) = make_float4(u[t].x, u[t].y, u[t + 1].x, u[t + 1].y);
-      } else {
+        for (int c = 0; c < 8; ++c) u[r2][c] = tb[r_ * TS + a_ + A * c];
+      }
 #pragma unroll
-        for (int t = 0; t < T; ++t) dst[t] = u[t];
+      for (int r2 = 0; r2 < RPT; ++r2) {
+        dft8<-1>(u[r2]);  // twiddle w_M^{t a} deferred to the reduction (FMA-fused)
+        float2* dst = redt(r2) + r_ * RS + a_ * RT;
+        if constexpr (T % 2 == 0) {
+#pragma unroll
+          for (int t = 0; t < T; t += 2)
+            *reinterpret_cast<float4*>(dst + t) = make_float4(u[r2][t].x, u[r2][t].y, u[r2][t + 1].x, u[r2][t + 1].y);
+        } else {
+#pragma unroll
+          for (int t = 0; t < T; ++t) dst[t] = u[r2][t];
+        }
       }
     }
     team_sync<M>(team);
     // ---- sum over a: X[r + 8t] for the thread's storage column q' = tt
     if (tt < KY) {
-      float2 part[A];
+      float2 part[RPT][A];
 #pragma unroll
-      for (int a = 0; a < A; ++a) part[a] = redt[rq * RS + a * RT + tq];
-      // sum_a w_M^{tq a} part[a]: two interleaved FMA chains, then one add
-      float2 s0 = part[0], s1 = make_float2(0.f, 0.f);
+      for (int r2 = 0; r2 < RPT; ++r2) {
+        const float2* rb = redt(r2);
 #pragma unroll
-      for (int a = 1; a < A; ++a) {
-        if (a & 1)
-          cmac(s1, part[a], tw3[a]);
-        else
-          cmac(s0, part[a], tw3[a]);
+        for (int a = 0; a < A; ++a) part[r2][a] = rb[rq * RS + a * RT + tq];
       }
-      const float2 sacc = cadd(s0, s1);
-      const int x1 = j * TEAMS + team;
-      Tc[x1 * KY + tt] = sacc;
+#pragma unroll
+      for (int r2 = 0; r2 < RPT; ++r2) {
+        // sum_a w_M^{tq a} part[a]: two interleaved FMA chains, then one add
+        float2 s0 = part[r2][0], s1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int a = 1; a < A; ++a) {
+          if (a & 1)
+            cmac(s1, part[r2][a], tw3[a]);
+          else
+            cmac(s0, part[r2][a], tw3[a]);
+        }
+        const int x1 = j * ROWS + team + TEAMS * r2;
+        Tc[x1 * KY + tt] = cadd(s0, s1);
+      }
     }
     if (++slot == S) {
       slot = 0;
@@ -446,7 +472,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
 // ---------------------------------------------------------------- dispatch
 template <class G>
 constexpr size_t fwd_smem(int S, bool dld = false) {
-  return sizeof(float2) * ((size_t)(dld ? 0 : S) * G::TEAMS * G::NY + G::TEAMS * 8 * (G::TS + G::RS) +
+  return sizeof(float2) * ((size_t)(dld ? 0 : S) * G::ROWS * G::NY + G::ROWS * 8 * (G::TS + G::RS) +
                            G::KX * G::KY + G::NY + G::DX) +
          16 * S + 64;
 }
@@ -504,10 +530,15 @@ static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, cons
 template <class G, int S>
 static cudaError_t launch_fwd(const float2* x, float2* A, int64_t planes, const float2* tw, bool natural,
                               cudaStream_t st) {
-  const bool dld = (plane_variant<G>() & 2) != 0;
-  if (natural)
-    return dld ? launch_fwd_v<G, S, true, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, true, false>(x, A, planes, tw, st);
-  return dld ? launch_fwd_v<G, S, false, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, false, false>(x, A, planes, tw, st);
+  if constexpr (G::RPT > 1) {  // interleaved rows come from the TMA ring only
+    return natural ? launch_fwd_v<G, S, true, false>(x, A, planes, tw, st)
+                   : launch_fwd_v<G, S, false, false>(x, A, planes, tw, st);
+  } else {
+    const bool dld = (plane_variant<G>() & 2) != 0;
+    if (natural)
+      return dld ? launch_fwd_v<G, S, true, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, true, false>(x, A, planes, tw, st);
+    return dld ? launch_fwd_v<G, S, false, true>(x, A, planes, tw, st) : launch_fwd_v<G, S, false, false>(x, A, planes, tw, st);
+  }
 }
 
 template <class G, int SO, bool NAT, bool DST>
@@ -536,11 +567,11 @@ static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const
              : launch_inv_v<G, SO, false, false>(Cm, y, planes, tw, scale, st);
 }
 
-template <class G, int S, int SO>
+template <class G, int S, int SO, class GF = G>
 static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
                             const float2* tw, int prec, void* wimg, cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
-  cudaError_t e = launch_fwd<G, S>(x, A, B * H, tw, false, st);
+  cudaError_t e = launch_fwd<GF, S>(x, A, B * H, tw, false, st);
   if (e != cudaSuccess) return e;
   if (mark) mark(st);
   // channel mixing over modes, 1/(dx*dy) folded into alpha
@@ -555,11 +586,23 @@ static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w,
 }
 
 using G512 = PlaneGeo<512, 64, 512, 64, 512>;
+// forward of the 512 geometry: 4 teams x 2 interleaved rows (ILP against the
+// shared-memory latency that bounds the packed-math forward), same smem
+using G512f = PlaneGeo<512, 64, 512, 64, 256, 2>;
+static bool fwd_rpt2() {  // TFNO_PLANE_RPT=1 selects the 8-team / 1-row forward (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFNO_PLANE_RPT");
+    v = e ? atoi(e) : 2;
+  }
+  return v != 1;
+}
 using G256a = PlaneGeo<256, 32, 256, 32, 512>;
 using G256b = PlaneGeo<256, 16, 256, 16, 512>;
 using G128 = PlaneGeo<128, 16, 128, 16, 256>;
 
 static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
+static_assert(fwd_smem<G512f>(3) <= 227 * 1024, "smem");
 static_assert(inv_smem<G512>(3) <= 227 * 1024, "smem");
 
 bool plane2d_supported(const tfno_cfg* c) {
@@ -573,7 +616,7 @@ cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes
                                cudaStream_t st) {
   const int dx = c->dim_x, kx = c->keep_x;
   const int64_t P = (int64_t)c->batch * c->hidden_dim;
-  if (dx == 512) return launch_fwd<G512, 3>(x, modes, P, tw, true, st);
+  if (dx == 512) return fwd_rpt2() ? launch_fwd<G512f, 3>(x, modes, P, tw, true, st) : launch_fwd<G512, 3>(x, modes, P, tw, true, st);
   if (dx == 256 && kx == 32) return launch_fwd<G256a, 4>(x, modes, P, tw, true, st);
   if (dx == 256 && kx == 16) return launch_fwd<G256b, 4>(x, modes, P, tw, true, st);
   if (dx == 128) return launch_fwd<G128, 4>(x, modes, P, tw, true, st);
@@ -595,7 +638,9 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
                                  float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t st,
                                  void (*mark)(cudaStream_t)) {
   const int dx = c->dim_x, kx = c->keep_x;
-  if (dx == 512) return run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  if (dx == 512)
+    return fwd_rpt2() ? run_pair<G512, 3, 3, G512f>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
+                      : run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);

@@ -174,11 +174,14 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
 // consumed from shared memory (double buffer).
 // TI x TJ = 8 x 8 (128 x 128 tile, BK = 8, one CTA of 200+ registers per
 // SM) halves the shared-memory operand loads per FFMA for large M and N.
-template <int TI, int TJ>
+// PK: packed f32x2 form — the W chunk is staged as (wr, wi, -wi, wr) so one
+// complex MAC is two FFMA2 with broadcast A operands (half the issue slots of
+// the 4-FFMA form at the same FP32-pipe rate).
+template <int TI, int TJ, bool PK = false>
 __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kernel(GemmArgs g) {
-  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 ? 8 : 16);
+  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 || PK ? 8 : 16);
   __shared__ __align__(16) float2 As[2][FBK][FBM];
-  __shared__ __align__(16) float2 Ws[2][FBK][FBN];
+  __shared__ __align__(16) float2 Ws[2][FBK][FBN * (PK ? 2 : 1)];
   const int tid = threadIdx.x;
   const int tm = tid % 16, tn = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
@@ -233,7 +236,14 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
       const int i = tid + r * 256;
-      *reinterpret_cast<float4*>(&Ws[buf][i / (FBN / 2)][(i % (FBN / 2)) * 2]) = rw[r];
+      const float4 w = rw[r];
+      if constexpr (PK) {  // (wr, wi, -wi, wr) per complex W element
+        float4* d = reinterpret_cast<float4*>(&Ws[buf][i / (FBN / 2)][(i % (FBN / 2)) * 4]);
+        d[0] = make_float4(w.x, w.y, -w.y, w.x);
+        d[1] = make_float4(w.z, w.w, -w.w, w.z);
+      } else {
+        *reinterpret_cast<float4*>(&Ws[buf][i / (FBN / 2)][(i % (FBN / 2)) * 2]) = w;
+      }
     }
   };
   float2 acc[TI][TJ];
@@ -253,12 +263,25 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
       float2 av[TI], bv[TJ];
 #pragma unroll
       for (int i = 0; i < TI; ++i) av[i] = As[buf][kk][tm + 16 * i];
+      if constexpr (PK) {
+        float4 bq[TJ];
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) bq[j] = *reinterpret_cast<const float4*>(&Ws[buf][kk][2 * (tn + 16 * j)]);
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+          for (int j = 0; j < TJ; ++j) {
+            acc[i][j] = fma2(make_float2(av[i].x, av[i].x), make_float2(bq[j].x, bq[j].y), acc[i][j]);
+            acc[i][j] = fma2(make_float2(av[i].y, av[i].y), make_float2(bq[j].z, bq[j].w), acc[i][j]);
+          }
+      } else {
 #pragma unroll
       for (int j = 0; j < TJ; ++j) bv[j] = Ws[buf][kk][tn + 16 * j];
 #pragma unroll
       for (int i = 0; i < TI; ++i)
 #pragma unroll
         for (int j = 0; j < TJ; ++j) cmac_s(acc[i][j], av[i], bv[j]);
+      }
     }
     if (more) {
       store_chunk(buf ^ 1);
@@ -440,6 +463,11 @@ static void launch3m(dim3 grid, const GemmArgs& g, cudaStream_t s) {
   cgemm3m_modes_kernel<TI, TJ><<<grid, 256, cgemm3m_smem<TI, TJ>(), s>>>(g);
 }
 
+static bool gemm_packed() {  // TFNO_CGEMM_PACKED=0 selects the scalar 4-FFMA inner loop (A/B)
+  const char* e = getenv("TFNO_CGEMM_PACKED");
+  return e ? atoi(e) != 0 : true;
+}
+
 static int gemm_algo() {  // TFNO_CGEMM_ALGO: 4 = classic 4M product (default), 3 = Gauss 3M (read per call)
   const char* e = getenv("TFNO_CGEMM_ALGO");
   return e ? atoi(e) : 4;
@@ -485,10 +513,13 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
     launch3m<8, 4>(grid, g, s);
   } else if (fast && g.N > 64 && g.M >= 128 && big_tiles()) {
     dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
-    cgemm_modes_kernel<8, 8><<<grid, 256, 0, s>>>(g);
+    if (gemm_packed())
+      cgemm_modes_kernel<8, 8, true><<<grid, 256, 0, s>>>(g);
+    else
+      cgemm_modes_kernel<8, 8><<<grid, 256, 0, s>>>(g);
   } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
-    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);
+    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);  // packed form spills at 2 CTAs/SM
   } else if (fast && g.M >= 128) {
     dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
     cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(g);

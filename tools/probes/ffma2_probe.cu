@@ -18,9 +18,16 @@ __global__ void k(float* out, int iters, float s) {
     } else if (MODE == 1) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(p[i]) : "l"(ss));
-    } else {
+    } else if (MODE == 2) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[i]) : "l"(ss));
+    } else {
+      // FFMA2 with a broadcast operand: (a, a) * p + p
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float bx = a[i];
+        asm volatile("{.reg .b64 t; mov.b64 t, {%1, %1}; fma.rn.f32x2 %0, t, %0, %2;}" : "+l"(p[i]) : "f"(bx), "l"(ss));
+      }
     }
   }
   float r = 0.f;
@@ -32,17 +39,18 @@ int main() {
   float* out; cudaMalloc(&out, 148 * 8 * 1024 * sizeof(float));
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int iters = 20000;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (mode == 0) k<0><<<148 * 8, 256>>>(out, iters, 0.999f);
       if (mode == 1) k<1><<<148 * 8, 256>>>(out, iters, 0.999f);
       if (mode == 2) k<2><<<148 * 8, 256>>>(out, iters, 0.999f);
+      if (mode == 3) k<3><<<148 * 8, 256>>>(out, iters, 0.999f);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);
       double flops = 148.0 * 8 * 256 * iters * 16 * (mode == 2 ? 1 : 2);
       if (rep) printf("%s: %.3f ms  %.1f TFLOP/s (fp32 lane-ops incl. FMA=2)\n",
-                      mode == 0 ? "FFMA scalar" : mode == 1 ? "FFMA2 packed" : "FADD2 packed", ms, flops / ms / 1e9);
+                      mode == 0 ? "FFMA scalar" : mode == 1 ? "FFMA2 packed" : mode == 2 ? "FADD2 packed" : "FFMA2 bcast", ms, flops / ms / 1e9);
     }
   }
   return 0;

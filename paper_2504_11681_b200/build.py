@@ -52,6 +52,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [nvcc, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
         else:
             cmd = [nvcc] + NVCC_FLAGS + ["-I", INCLUDE, "-c", path, "-o", obj]
+            # A/B hook: TFNO_SCALAR_FILES=a.cu,b.cu builds those files with the scalar complex primitives
+            if src in os.environ.get("TFNO_SCALAR_FILES", "").split(","):
+                cmd.insert(1, "-DTFNO_SCALAR_COMPLEX")
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

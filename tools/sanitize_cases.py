@@ -35,6 +35,21 @@ for shape, modes in cases:
         T.run_layer_device(cfg, x, w, mode=mode)
         torch.cuda.synchronize()
         print("ok", shape, mode, flush=True)
+for shape in ((2, 8, 8, 512, 512, 64, 64, 2), (3, 12, 20, 1, 1024, 1, 128, 1)):  # tcgen05 layer (W' image)
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = rnd(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), rnd(cfg.hidden_dim, cfg.output_dim)
+    for prec in ("tf32x3", "tf32"):
+        T.run_layer_device(cfg, x, w, mode="fully_fused", precision=prec)
+        torch.cuda.synchronize()
+        print("ok tc layer", shape, prec, flush=True)
+from paper_2504_11681_b200.autograd import layer_backward  # noqa: E402
+from paper_2504_11681_b200.symmetric import run_layer_symmetric  # noqa: E402
+cfg = T.FnoLayerConfig(2, 4, 6, 64, 64, 8, 8, 2)
+x, w, gy = rnd(2, 4, 64, 64), rnd(4, 6), rnd(2, 6, 64, 64)
+layer_backward(cfg, x, w, gy)
+run_layer_symmetric(cfg, x, w)
+torch.cuda.synchronize()
+print("ok backward / symmetric", flush=True)
 for prec in ("tf32", "tf32x3", "bf16"):
     A = rnd(2, 64, 256).transpose(1, 2)
     T.cgemm_device(A, rnd(64, 96), precision=prec)

@@ -567,7 +567,7 @@ static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const
              : launch_inv_v<G, SO, false, false>(Cm, y, planes, tw, scale, st);
 }
 
-template <class G, int S, int SO, class GF = G>
+template <class G, int S, int SO, class GF = G, class GI = G>
 static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
                             const float2* tw, int prec, void* wimg, cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
@@ -580,7 +580,7 @@ static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w,
   ga.wimg = wimg;
   if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e;
   if (mark) mark(st);
-  if ((e = launch_inv<G, SO>(Cm, y, B * N, tw, 1.0f, false, st)) != cudaSuccess) return e;
+  if ((e = launch_inv<GI, SO>(Cm, y, B * N, tw, 1.0f, false, st)) != cudaSuccess) return e;
   if (mark) mark(st);
   return cudaSuccess;
 }
@@ -599,6 +599,24 @@ static bool fwd_rpt2() {  // TFNO_PLANE_RPT=1 selects the 8-team / 1-row forward
 }
 using G256a = PlaneGeo<256, 32, 256, 32, 512>;
 using G256b = PlaneGeo<256, 16, 256, 16, 512>;
+// half-thread inverses (fewer teams -> fewer idle threads in the column passes
+// between the class barriers); A/B with TFNO_PLANE_INV_HALF=0/1
+using G256b8 = PlaneGeo<256, 16, 256, 16, 256>;
+using G256a8 = PlaneGeo<256, 32, 256, 32, 256>;
+using G512i = PlaneGeo<512, 64, 512, 64, 256>;
+static int inv_half_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFNO_PLANE_INV_HALF");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+// measured (profiles/r01/plane_variants.txt): C5 1.753 -> 1.493 ms, C3 0.202 -> 0.187 ms,
+// C4 5.62 -> 7.44 ms (worse: 512 geometry keeps 8 teams)
+static bool inv256b_8() { return inv_half_env() != 0; }
+static bool inv256a_8() { return inv_half_env() != 0; }
+static bool inv512_half() { return inv_half_env() == 2; }
 using G128 = PlaneGeo<128, 16, 128, 16, 256>;
 
 static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
@@ -638,11 +656,17 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
                                  float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t st,
                                  void (*mark)(cudaStream_t)) {
   const int dx = c->dim_x, kx = c->keep_x;
-  if (dx == 512)
+  if (dx == 512) {
+    if (inv512_half()) return run_pair<G512, 3, 3, G512f, G512i>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
     return fwd_rpt2() ? run_pair<G512, 3, 3, G512f>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
                       : run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  if (dx == 256 && kx == 32) return run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  if (dx == 256 && kx == 16) return run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  }
+  if (dx == 256 && kx == 32)
+    return inv256a_8() ? run_pair<G256a, 4, 2, G256a, G256a8>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
+                       : run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
+  if (dx == 256 && kx == 16)
+    return inv256b_8() ? run_pair<G256b, 4, 2, G256b, G256b8>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
+                       : run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
   return cudaErrorNotSupported;
 }

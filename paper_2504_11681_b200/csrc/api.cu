@@ -196,10 +196,11 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
   // tensor-core precisions on contraction-heavy shapes: the fused 1D kernel's
   // contraction is FP32 SIMT, so the unfused schedule with the tcgen05 CGEMM wins
   const bool tc_heavy = prec != TFNO_FP32 && g.H * g.N >= 128 * 128;
-  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy &&
-      fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N)) {
+  const bool f1_full = fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N);
+  const int f1_forced = f1_full ? 0 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
+  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1)) {
     s.f1 = true;
-    s.f1_cluster = fused1d_cluster((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
+    s.f1_cluster = f1_full ? fused1d_cluster((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx) : 1;
     s.f1_split = s.f1_cluster > 1 ? 1 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
     s.fg = s.gi = true;
     s.need_s1 = s.need_mid = (g.rank == 2);

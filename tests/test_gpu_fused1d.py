@@ -41,6 +41,7 @@ CASES = [
     (2, 64, 64, 4, 256, 2, 32, 2),       # rank 2: x passes around the fused rows
     (16, 64, 64, 1, 128, 1, 32, 1),      # C1 exactly: N = 128 rows (16 lanes x 8), split 4
     (3, 32, 64, 1, 128, 1, 20, 1),       # N = 128, ragged keep
+    (4, 128, 128, 1, 1024, 1, 128, 1),   # N_out 128 at N = 1024: forced output split (2 x 64)
 ]
 
 

@@ -30,7 +30,9 @@ class FnoChain:
         dev = self.weights[0].device
         shape = (cfg.batch, cfg.output_dim, cfg.dim_x, cfg.dim_y)
         self.buf = [t.empty(shape, dtype=t.complex64, device=dev), t.empty(shape, dtype=t.complex64, device=dev)]
-        _device.workspace(workspace_bytes(cfg, mode, precision), dev)  # allocate before any capture
+        # the chain owns its workspace: a captured graph keeps this pointer, independent of the
+        # shared scratch other calls may regrow
+        self.ws = t.empty(max(workspace_bytes(cfg, mode, precision), 1), dtype=t.uint8, device=dev)
         self.graph = None
         self._x = None
 
@@ -39,7 +41,7 @@ class FnoChain:
         for i, w in enumerate(self.weights):
             out = self.buf[i % 2]
             run_layer_device(self.cfg, cur, w, mode=self.mode, precision=self.precision, out=out,
-                             stream=stream, validate=(i == 0))
+                             stream=stream, validate=(i == 0), workspace=self.ws)
             cur = out
         return cur
 

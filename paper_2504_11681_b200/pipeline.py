@@ -203,10 +203,13 @@ def layer_schedule(cfg: FnoLayerConfig, mode: str = "fully_fused", precision: st
 
 def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILES, mode: str = "fully_fused",
                      fft_batch_size: int = FFT_BLOCK_BATCH, out=None, precision: str = "fp32", stream=None,
-                     validate: bool = True):
+                     validate: bool = True, workspace=None):
     """Device API: x [B,H,dx,dy] and w [H,N] complex64 CUDA tensors (w in
     row-major [H][N]); returns the [B,N,dx,dy] CUDA tensor.  Asynchronous
-    on ``stream`` (default: torch's current stream)."""
+    on ``stream`` (default: torch's current stream).  ``workspace``: an
+    optional caller-owned uint8 CUDA tensor (``workspace_bytes`` large) —
+    CUDA graphs capture its pointer, so graph owners pass their own instead
+    of the shared per-device scratch (which may be regrown by other calls)."""
     t = _device.torch()
     if validate:
         _validate(cfg, tuple(x.shape), tuple(w.shape), tiles, mode, fft_batch_size)
@@ -222,7 +225,10 @@ def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILE
     c = cfg_struct(cfg)
     mcode, pcode = MODE_CODES[mode], PREC_CODES[precision]
     nbytes = int(lib().tfno_workspace_bytes(ctypes.byref(c), mcode, pcode))
-    ws = _device.workspace(nbytes, dev)
+    if workspace is not None and workspace.numel() >= nbytes:
+        ws = workspace if nbytes else None
+    else:
+        ws = _device.workspace(nbytes, dev)
     rc = lib().tfno_layer_forward(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                   ws.data_ptr() if ws is not None else None, nbytes,
                                   _device.stream_ptr(stream))

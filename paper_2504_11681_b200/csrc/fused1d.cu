@@ -62,6 +62,7 @@ struct F1Geo {
   // register split (setmaxnreg) inside the CTA's launch allocation of 640 x 96:
   // producer warpgroup 24, FFT warps 96 (unchanged), GEMM warps 128
   // (L = 32 rows hold 32 complex values per lane: FFT warps get 112, GEMM warps 112)
+  // (an 88 / 136 split for the large tiles measured no faster: N256 H256 0.541 ms either way)
   static constexpr int REG_LAUNCH = 96, REG_PROD = 24, REG_FFT = L == 32 ? 112 : 96, REG_GEMM = L == 32 ? 112 : 128;
   static_assert(128 * REG_PROD + NFT * REG_FFT + NGT * REG_GEMM <= NTH * REG_LAUNCH, "register pool");
 };
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
 
   // ================= FFT warps
   if constexpr (G::REG_FFT > G::REG_LAUNCH) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
+  if constexpr (G::REG_FFT < G::REG_LAUNCH) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_FFT));
   const int64_t nmine = (items - first + units - 1) / units;  // grid <= items
   const int lane = tid % L, team = tid / L;
   const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (team & 1)));

@@ -229,6 +229,8 @@ def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILE
         ws = workspace if nbytes else None
     else:
         ws = _device.workspace(nbytes, dev)
+        if ws is not None and stream is not None:
+            ws.record_stream(stream)  # a later regrowth must not recycle it under this stream's kernels
     rc = lib().tfno_layer_forward(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                   ws.data_ptr() if ws is not None else None, nbytes,
                                   _device.stream_ptr(stream))

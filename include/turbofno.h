@@ -143,6 +143,20 @@ int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* 
 int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, const void* in, void* out,
                   float scale, void* stream);
 
+/* Real-field FNO block (extension beyond the reference, which is complex-to-complex only).
+ * The real layer irfft2(rfft2(x)[:kx, :ky] W, s=(dx, dy)), ky <= dy/2 + 1, is composed on the
+ * spectrum ABI: tfno_real_to_complex -> tfno_spectrum_forward -> tfno_half_spectrum_weight ->
+ * tfno_cgemm -> tfno_spectrum_inverse -> tfno_real_epilogue (see paper_2504_11681_b200/realfield.py).
+ *   tfno_real_to_complex:      z[i] = x[i] + 0i, n reals (16-byte aligned pointers)
+ *   tfno_half_spectrum_weight: modes[r][k] *= 2 for 0 < k < dy/2 (rows x ky complex, in place)
+ *   tfno_real_epilogue:        out[b][n][p] = act(Re z[b][n][p] + bypass[b][n][p] + bias[n]);
+ *                              bypass / bias may be NULL; activation TFNO_ACT_*. */
+enum { TFNO_ACT_NONE = 0, TFNO_ACT_RELU = 1, TFNO_ACT_GELU = 2 };
+int tfno_real_to_complex(const float* x, void* z, int64_t n, void* stream);
+int tfno_half_spectrum_weight(void* modes, int64_t rows, int ky, int dy, void* stream);
+int tfno_real_epilogue(const void* z, const float* bypass, const float* bias, int64_t batch, int N, int64_t P,
+                       int activation, float* out, void* stream);
+
 /* Kernels of this library launched by the calling thread since load (library
  * kernels of the staged baseline, cuFFT/cuBLAS, are not counted). */
 long long tfno_launch_count(void);

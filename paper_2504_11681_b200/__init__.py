@@ -22,5 +22,6 @@ from .pipeline import (ARRAY_NAMES, MODES, ConfigMismatch, FusedSchedule, Schedu
                        traffic_delta, workspace_bytes)
 
 from .autograd import layer_backward, spectral_layer  # noqa: F401,E402  (backward pass, §8f row 4)
+from .realfield import fno_block, real_layer  # noqa: F401,E402  (R2C/C2R layer, bypass + activation, §8f row 4)
 
 __version__ = "0.1.0"

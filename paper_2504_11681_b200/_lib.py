@@ -56,6 +56,9 @@ _SIGS = {
                                        _VP, _I64, _I64, _I64, ctypes.c_float, ctypes.c_int, _VP]),
     "tfno_modulate": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      _VP, _VP, ctypes.c_float, _VP]),
+    "tfno_real_to_complex": (ctypes.c_int, [_VP, _VP, _I64, _VP]),
+    "tfno_half_spectrum_weight": (ctypes.c_int, [_VP, _I64, ctypes.c_int, ctypes.c_int, _VP]),
+    "tfno_real_epilogue": (ctypes.c_int, [_VP, _VP, _VP, _I64, ctypes.c_int, _I64, ctypes.c_int, _VP, _VP]),
     "tfno_launch_count": (ctypes.c_longlong, []),
     "tfno_set_stage_events": (None, [_VP, ctypes.c_int]),
     "tfno_layer_schedule": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int,

@@ -50,6 +50,13 @@ layer_backward(cfg, x, w, gy)
 run_layer_symmetric(cfg, x, w)
 torch.cuda.synchronize()
 print("ok backward / symmetric", flush=True)
+for shape in ((2, 4, 6, 64, 64, 8, 8, 2), (3, 2, 3, 1, 2, 1, 2, 1)):  # real layer + block epilogue (vector/scalar)
+    cfg = T.FnoLayerConfig(*shape)
+    xr = torch.randn(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y, device="cuda")
+    T.fno_block(cfg, xr, rnd(cfg.hidden_dim, cfg.output_dim), bypass_w=torch.randn(cfg.hidden_dim, cfg.output_dim,
+                device="cuda"), bias=torch.randn(cfg.output_dim, device="cuda"), activation="gelu")
+    torch.cuda.synchronize()
+    print("ok real block", shape, flush=True)
 for prec in ("tf32", "tf32x3", "bf16"):
     A = rnd(2, 64, 256).transpose(1, 2)
     T.cgemm_device(A, rnd(64, 96), precision=prec)

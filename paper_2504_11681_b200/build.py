@@ -55,6 +55,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             # A/B hook: TFNO_SCALAR_FILES=a.cu,b.cu builds those files with the scalar complex primitives
             if src in os.environ.get("TFNO_SCALAR_FILES", "").split(","):
                 cmd.insert(1, "-DTFNO_SCALAR_COMPLEX")
+            # A/B hook: TFNO_NVCC_DEFS=A,B adds -DA -DB to every CUDA translation unit
+            for d in filter(None, os.environ.get("TFNO_NVCC_DEFS", "").split(",")):
+                cmd.insert(1, "-D" + d)
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

@@ -33,6 +33,29 @@
 namespace tfno {
 
 template <int L, int V, int KP, int TI, int TJ, int NOUT>
+struct F1Geo;
+
+// A element e of the chunk ring: a (AW = 1) or (a.x, a.y, -a.y, a.x) (AW = 2)
+template <int AW>
+__device__ __forceinline__ void put_a(float2* As, int e, float2 a) {
+  if constexpr (AW == 2)
+    reinterpret_cast<float4*>(As)[e] = make_float4(a.x, a.y, -a.y, a.x);
+  else
+    As[e] = a;
+}
+
+// acc += a * b with a staged as (a.x, a.y, -a.y, a.x): acc += b.x * a + b.y * (-a.y, a.x)
+__device__ __forceinline__ void cmac_comp(float2& acc, float4 a, float2 b) {
+#ifdef TFNO_SCALAR_COMPLEX
+  acc.x = fmaf(b.y, a.z, fmaf(b.x, a.x, acc.x));
+  acc.y = fmaf(b.y, a.w, fmaf(b.x, a.y, acc.y));
+#else
+  acc = fma2(make_float2(b.x, b.x), make_float2(a.x, a.y), acc);
+  acc = fma2(make_float2(b.y, b.y), make_float2(a.z, a.w), acc);
+#endif
+}
+
+template <int L, int V, int KP, int TI, int TJ, int NOUT>
 struct F1Geo {
   // N = L * V: L lanes per row team, V values per lane (V = L: square rows N = 256 / 1024;
   // V = 8 with L = 16: N = 128)
@@ -43,17 +66,28 @@ struct F1Geo {
   static_assert(MT * NTG == NGT, "GEMM thread grid must cover the GEMM warps");
   static_assert(NOUT % TEAMS == 0, "inverse rows per team");
   static constexpr int BAR_BYTES = 2048;  // >= 8 * (2 * TEAMS * NSLOT + 2 + 2 + 2 * NA + 2)
-  // float2 units after the barrier block; NSLOT input-row slots per team
-  static constexpr size_t total(int ns) {
-    return (size_t)TEAMS * N * ns + 2 * KC * NOUT + NA * KC * KT + KT * NOUT + TEAMS * N + N + L;
+  // float2 units after the barrier block; NSLOT input-row slots per team; AW float2 per A element
+  static constexpr size_t total_aw(int ns, int aw) {
+    return (size_t)TEAMS * N * ns + 2 * KC * NOUT + NA * KC * KT * aw + KT * NOUT + TEAMS * N + N + L;
   }
+  // A elements staged with their companion (a.x, a.y, -a.y, a.x) when it fits: the GEMM
+  // warps then issue only FFMA2 (b.x broadcast * a, b.y broadcast * companion) -- without it
+  // ptxas builds (-b.y, b.x) pairs with MOV / FADD, ~0.6 extra issue slots per FFMA2
+#ifdef TFNO_F1_NO_ACOMP
+  static constexpr int AW = 1;
+#else
+  // (only where it does not cost an input-row slot)
+  static constexpr int NS1 = (BAR_BYTES + 8 * total_aw(4, 1) <= 220 * 1024) ? 4 : (BAR_BYTES + 8 * total_aw(2, 1) <= 220 * 1024) ? 2 : 1;
+  static constexpr int AW = (BAR_BYTES + 8 * total_aw(NS1, 2) <= 220 * 1024) ? 2 : 1;
+#endif
+  static constexpr size_t total(int ns) { return total_aw(ns, AW); }
   // input-row slots per team: as deep a prefetch as fits (4 rows in flight per team at N <= 256)
   static constexpr int NSLOT = (BAR_BYTES + 8 * total(4) <= 220 * 1024) ? 4 : (BAR_BYTES + 8 * total(2) <= 220 * 1024) ? 2 : 1;
   static_assert(8 * (2 * TEAMS * NSLOT + 4 + 2 * NA + 2) <= BAR_BYTES, "mbarrier block");
   static constexpr int OFF_SLOT = 0;
   static constexpr int OFF_W = OFF_SLOT + TEAMS * N * NSLOT;
   static constexpr int OFF_A = OFF_W + 2 * KC * NOUT;
-  static constexpr int OFF_C = OFF_A + NA * KC * KT;
+  static constexpr int OFF_C = OFF_A + NA * KC * KT * AW;
   static constexpr int OFF_TR = OFF_C + KT * NOUT;
   static constexpr int OFF_TWN = OFF_TR + TEAMS * N;
   static constexpr int OFF_TWL = OFF_TWN + N;
@@ -231,19 +265,36 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         const int s = (int)(kk % NA), ws = (int)(kk & 1);
         mbar_wait(&afull[s], (uint32_t)((kk / NA) & 1));
         mbar_wait(&wfull[ws], (uint32_t)((kk >> 1) & 1));
-        const float2* Ab = As + s * KC * KT;
         const float2* Wc = Wr + ws * KC * NOUT;
+        if constexpr (G::AW == 2) {
+          const float4* Ab = reinterpret_cast<const float4*>(As) + s * KC * KT;
 #pragma unroll 4
-        for (int hl = 0; hl < KC; ++hl) {
-          float2 av[TI], bv[TJ];
+          for (int hl = 0; hl < KC; ++hl) {
+            float4 av[TI];
+            float2 bv[TJ];
 #pragma unroll
-          for (int i = 0; i < TI; ++i) av[i] = Ab[hl * KT + tm + MT * i];
+            for (int i = 0; i < TI; ++i) av[i] = Ab[hl * KT + tm + MT * i];
 #pragma unroll
-          for (int j = 0; j < TJ; ++j) bv[j] = Wc[hl * NOUT + tn + NTG * j];
+            for (int j = 0; j < TJ; ++j) bv[j] = Wc[hl * NOUT + tn + NTG * j];
 #pragma unroll
-          for (int i = 0; i < TI; ++i)
+            for (int i = 0; i < TI; ++i)
 #pragma unroll
-            for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+              for (int j = 0; j < TJ; ++j) cmac_comp(acc[i][j], av[i], bv[j]);
+          }
+        } else {
+          const float2* Ab = As + s * KC * KT;
+#pragma unroll 4
+          for (int hl = 0; hl < KC; ++hl) {
+            float2 av[TI], bv[TJ];
+#pragma unroll
+            for (int i = 0; i < TI; ++i) av[i] = Ab[hl * KT + tm + MT * i];
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) bv[j] = Wc[hl * NOUT + tn + NTG * j];
+#pragma unroll
+            for (int i = 0; i < TI; ++i)
+#pragma unroll
+              for (int j = 0; j < TJ; ++j) cmac(acc[i][j], av[i], bv[j]);
+          }
         }
         __syncwarp();
         if ((gt & 31) == 0) {
@@ -309,11 +360,10 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         float2 o[KP];
         wf::dftL_first<L, KP>(v, o, twL);
         if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
-        float2* Ab = As + s * KC * KT;
 #pragma unroll
         for (int k2 = 0; k2 < KP; ++k2) {
           const int q = lane + L * k2;
-          Ab[team * KT + q] = q < keep ? o[k2] : make_float2(0.f, 0.f);
+          put_a<G::AW>(As, s * KC * KT + team * KT + q, q < keep ? o[k2] : make_float2(0.f, 0.f));
         }
         } else {
         // N = 128 = 16 lanes x 8: Y_t[k1] = DFT8_j x[t + 16 j] * w_128^{t k1};
@@ -346,12 +396,11 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
           v[k2] = cadd(v[k2], p);
         }
         if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
-        float2* Ab = As + s * KC * KT;
 #pragma unroll
         for (int k2 = 0; k2 < K2; ++k2) {
           if ((k2 & 1) != hf) continue;
           const int q = k1 + 8 * k2;
-          Ab[team * KT + q] = q < keep ? v[k2] : make_float2(0.f, 0.f);
+          put_a<G::AW>(As, s * KC * KT + team * KT + q, q < keep ? v[k2] : make_float2(0.f, 0.f));
         }
         }
         __syncwarp(tmask);

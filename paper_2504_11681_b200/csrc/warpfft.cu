@@ -15,9 +15,11 @@
 // No CTA barriers: every row lives in one (half-)warp (__syncwarp only).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 #include "wf_dft.cuh"
 
 namespace tfno {
@@ -382,7 +384,7 @@ struct TfGeo {
 template <int U, int K2>
 __global__ void __launch_bounds__(512, 1) team_fft_fwd_kernel(const float2* __restrict__ in, int64_t in_stride,
                                                             float2* __restrict__ out, int64_t out_stride, int64_t P,
-                                                            int keep, const float2* __restrict__ twg) {
+                                                            int keep, const float2* __restrict__ twg, int pfd) {
   using G = TfGeo<U>;
   constexpr int T = G::T, N = G::N;
   extern __shared__ __align__(16) float2 sm[];
@@ -407,6 +409,15 @@ __global__ void __launch_bounds__(512, 1) team_fft_fwd_kernel(const float2* __re
     const float2* src = in + (live ? row : 0) * in_stride;
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = live ? __ldg(&src[tt + T * j]) : make_float2(0.f, 0.f);
+    // pull the team's row pfd iterations ahead into L2 while this one computes
+    // (one CTA per SM: without it HBM idles during each row's transform)
+    if (pfd > 0 && tt == 0) {
+      const int64_t step = (int64_t)gridDim.x * G::TEAMS;
+      for (int d = (row0 == (int64_t)blockIdx.x * G::TEAMS) ? 1 : pfd; d <= pfd; ++d) {
+        const int64_t nr = row + d * step;
+        if (nr < P) l2_prefetch_bulk(in + nr * in_stride, N * sizeof(float2));
+      }
+    }
     wf::dftL<32, -1>(v, tw32);
 #pragma unroll
     for (int k1 = 1; k1 < 32; ++k1) v[k1] = cmul(v[k1], twN[G::swz(tt, k1)]);
@@ -548,7 +559,14 @@ static cudaError_t launch_tf(int dir, const float2* in, int64_t is, float2* out,
   if (dir < 0) {
     e = cudaFuncSetAttribute(team_fft_fwd_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    team_fft_fwd_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw);
+    static int pfd = -1;  // L2 prefetch distance in rows (TFNO_TEAM_PF; 0 = off)
+    if (pfd < 0) {
+      const char* env = getenv("TFNO_TEAM_PF");
+      pfd = env ? atoi(env) : 1;
+    }
+    // bulk prefetch needs 16-byte aligned rows
+    const int d = (((uintptr_t)in | (uintptr_t)(is * sizeof(float2))) & 15) ? 0 : pfd;
+    team_fft_fwd_kernel<U, K2><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw, d);
   } else {
     const size_t smem_i = G::smem_bytes(K2) <= 227 * 1024 ? G::smem_bytes(K2) : smem;
     e = cudaFuncSetAttribute(team_fft_inv_kernel<U, K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i);

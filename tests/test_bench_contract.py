@@ -36,3 +36,16 @@ def test_our_arm_needs_a_gpu():
         return
     r = _run(["--workload", "C1", "--steps", "1", "--warmup", "3", "--no-baselines", "--no-e2e", "--no-cpu"])
     assert r.returncode != 0
+
+
+def test_reference_arm_under_torchrun_world2():
+    """Driver launch for N > 1: rank 0 alone times the CPU reference and prints one line; rank 1 exits 0."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--workload", "C1", "--gpus", "2", "--steps", "1", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0

@@ -52,7 +52,13 @@ struct PlaneGeo {
   static constexpr int IPC = KX / ROWS;  // iterations per class
   static constexpr int PAD = ((-7 * A) % 16 + 16) % 16;
   static constexpr int RT = T + 2;                 // reduction buffer: padded t-stride
-  static constexpr int RS = A * RT + 8;            //                   per-r stride
+  // per-r stride, == T (mod 16 complex): the reduction reads (lane = rq*T + tq) then cover 32
+  // consecutive complex values modulo the 32 banks (256²/32: 4-way -> conflict-free); 512²/64 unchanged
+#ifdef TFNO_PLANE_RS_OLD
+  static constexpr int RS = A * RT + 8;
+#else
+  static constexpr int RS = A * RT + (((T - A * RT) % 16) + 16) % 16;
+#endif
   static constexpr int TS = M + PAD;  // transposed-row stride (== A mod 16: conflict-free reads)
   static constexpr int TASKS2 = (8 * KY + NTH - 1) / NTH;
   static_assert(A >= 1 && (1 << LOGA) == A, "A power of two");

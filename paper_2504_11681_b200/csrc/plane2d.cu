@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
       for (int tau = tid; tau < 8 * KY; tau += NTH) {
         const int q = tau % KY, s2 = tau / KY;
         float2 w[KA];
-#pragma unroll
         const int qi = NATURAL ? (q / T) + 8 * (q % T) : q;
+#pragma unroll
         for (int u = 0; u < KA; ++u) {
           const int p = s2 + 8 * u;
           w[u] = cmul(cin[p * KY + qi], twx[p * x0]);  // twx carries the output scale

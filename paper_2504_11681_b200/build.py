@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(BUILD_DIR, src + ".o")
         path = os.path.join(CSRC, src)
         if src.endswith(".cpp"):
-            cmd = [nvcc, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
+            cmd = [nvcc, "-O3", "-std=c++17", "-Wno-deprecated-gpu-targets", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
         else:
             cmd = [nvcc] + NVCC_FLAGS + ["-I", INCLUDE, "-c", path, "-o", obj]
             # A/B hook: TFNO_SCALAR_FILES=a.cu,b.cu builds those files with the scalar complex primitives

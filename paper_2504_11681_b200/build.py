@@ -22,7 +22,7 @@ BUILD_DIR = os.path.join(HERE, "_build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart", "shared",
               "-Xptxas", "-v"] + ARCH
-SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "fused1d.cu", "realfield.cu", "api.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "warpfft_fwd.cu", "fused1d.cu", "realfield.cu", "api.cu", "plan.cpp"]
 
 
 def _nvcc() -> str:

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "warpfft.cuh"
 #include "wf_dft.cuh"
 
 namespace tfno {
@@ -29,63 +30,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int L>
-struct WfGeo {
-  static constexpr int N = L * L;
-  static constexpr int NTH = 256;
-  static constexpr int ROWS = NTH / L;        // rows in flight per CTA pass
-  static constexpr int TSTR = L + 1;          // padded transpose stride (complex)
-  static constexpr size_t smem_bytes() {
-    return sizeof(float2) * ((size_t)L + (size_t)L * L + (size_t)ROWS * L * TSTR);
-  }
-};
-
-// forward: rows [P][src stride] -> out [P][keep] (out stride), src_len = N
-template <int L, int KP>
-__global__ void __launch_bounds__(WfGeo<L>::NTH) warp_fft_fwd_kernel(const float2* __restrict__ in,
-                                                                   int64_t in_stride, float2* __restrict__ out,
-                                                                   int64_t out_stride, int64_t P, int keep,
-                                                                   const float2* __restrict__ twg) {
-  using G = WfGeo<L>;
-  constexpr int N = G::N;
-  extern __shared__ __align__(16) float2 sm[];
-  float2* twL = sm;                 // w_L^k
-  float2* twN = twL + L;            // [k1][t] = w_N^{t k1}
-  float2* tr = twN + L * L;         // ROWS x L x TSTR
-  const int tid = threadIdx.x, lane = tid % L, rloc = tid / L;
-  const unsigned tmask = L == 32 ? 0xffffffffu : (0xffffu << (16 * (rloc & 1)));
-  for (int k = tid; k < L; k += G::NTH) twL[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / L)]);
-  for (int i = tid; i < L * L; i += G::NTH) {
-    const int k1 = i / L, t = i % L;
-    twN[i] = __ldg(&twg[(size_t)((t * k1) % N) * (TFNO_TW_MAX / N)]);
-  }
-  __syncthreads();
-  float2* trr = tr + rloc * L * G::TSTR;
-  for (int64_t row = (int64_t)blockIdx.x * G::ROWS + rloc; row < P; row += (int64_t)gridDim.x * G::ROWS) {
-    const float2* src = in + row * in_stride;
-    float2 v[L];
-#pragma unroll
-    for (int j = 0; j < L; ++j) v[j] = __ldg(&src[lane + L * j]);
-    wf::dftL<L, -1>(v, twL);
-#pragma unroll
-    for (int k1 = 1; k1 < L; ++k1) v[k1] = cmul(v[k1], twN[k1 * L + lane]);  // consecutive lanes
-    __syncwarp(tmask);
-#pragma unroll
-    for (int k1 = 0; k1 < L; ++k1) trr[k1 * G::TSTR + lane] = v[k1];
-    __syncwarp(tmask);
-    // lane = k1 now: gather Y_t[k1] over t, first KP outputs of DFT_L over t
-#pragma unroll
-    for (int t = 0; t < L; ++t) v[t] = trr[lane * G::TSTR + t];
-    float2 o[KP];
-    wf::dftL_first<L, KP>(v, o, twL);
-    float2* dst = out + row * out_stride;
-#pragma unroll
-    for (int k2 = 0; k2 < KP; ++k2) {
-      const int k = lane + L * k2;
-      if (k < keep) dst[k] = o[k2];
-    }
-  }
-}
 
 // inverse: modes [P][src_len] (src stride) -> rows [P][N] (out stride), x scale
 template <int L, int KP>
@@ -134,24 +78,6 @@ __global__ void __launch_bounds__(WfGeo<L>::NTH) warp_fft_inv_kernel(const float
 #pragma unroll
     for (int j = 0; j < L; ++j) dst[lane + L * j] = cscale(z[j], scale);
   }
-}
-
-template <int L, int KP>
-static cudaError_t launch_wf_fwd(const float2* in, int64_t is, float2* out, int64_t os, int64_t P, int keep,
-                                 const float2* tw, cudaStream_t s) {
-  using G = WfGeo<L>;
-  const size_t smem = G::smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(warp_fft_fwd_kernel<L, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t blocks = (P + G::ROWS - 1) / G::ROWS;
-  const int grid = (int)(blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8);
-  warp_fft_fwd_kernel<L, KP><<<grid, G::NTH, smem, s>>>(in, is, out, os, P, keep, tw);
-  ++g_launches;
-  return cudaGetLastError();
 }
 
 template <int L, int KP>
@@ -611,10 +537,9 @@ cudaError_t launch_warp_fft(int n, int dir, const float2* in, int64_t is, float2
   }
   const int L = n == 256 ? 16 : 32;
   const int kp = ((dir < 0 ? keep : src_len) + L - 1) / L;
-#define WF_CASE(LL, KK)                                                                        \
-  if (L == LL && kp == KK)                                                                     \
-    return dir < 0 ? launch_wf_fwd<LL, KK>(in, is, out, os, P, keep, tw, s)                    \
-                   : launch_wf_inv<LL, KK>(in, is, out, os, P, src_len, scale, tw, s);
+  if (dir < 0) return launch_warp_fft_fwd_rows(L, kp, in, is, out, os, P, keep, tw, s);  // warpfft_fwd.cu
+#define WF_CASE(LL, KK) \
+  if (L == LL && kp == KK) return launch_wf_inv<LL, KK>(in, is, out, os, P, src_len, scale, tw, s);
   WF_CASE(16, 1) WF_CASE(16, 2) WF_CASE(16, 3) WF_CASE(16, 4) WF_CASE(16, 5) WF_CASE(16, 6) WF_CASE(16, 7)
   WF_CASE(16, 8)
   WF_CASE(32, 1) WF_CASE(32, 2) WF_CASE(32, 3) WF_CASE(32, 4) WF_CASE(32, 5) WF_CASE(32, 6) WF_CASE(32, 7)

@@ -155,67 +155,158 @@ def load_traffic(workload, kernel):
         return None
 
 
-def cpu_reference(cfg_t, x_sample, w, workers):
-    """Time the oracle port (fnofuse restatement) on the host: returns (seconds, output)."""
-    from types import SimpleNamespace
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # pip --target install of the unmodified reference
 
-    from oracle import fnofuse_port as O
-    pool = O.CpuPool(workers)
-    cfg = SimpleNamespace(**cfg_t)
-    t0 = time.perf_counter()
-    out = pool.run(cfg, x_sample, w)
-    dt = time.perf_counter() - t0
-    pool.close()
-    return dt, out
+
+def workload_config(args, B, ws):
+    """The `config` object of the JSON line: identical in both arms (no product import)."""
+    _, H, N, dx, dy, kx, ky, rk, desc = WORKLOADS[args.workload]
+    io = 8 * B * H * dx * dy
+    return {"workload": desc, "batch_per_gpu": B, "global_batch": B * ws, "hidden": H, "out": N,
+            "dims": [dx, dy], "keep": [kx, ky], "rank": rk, "mode": args.mode, "precision": args.precision,
+            "parallelism": f"batch-sharded dp{ws}, no data-path collective",
+            "l2": (f"inputs larger than L2 ({io / 2**30:.1f} GiB per GPU); no flush" if io > (126 << 20) else
+                   f"inputs ({io / 2**20:.1f} MiB) fit in L2: L2-warm timing")}
+
+
+def reference_layer_flops(F, cfg):
+    """Canonical flops of one layer from the REFERENCE's own op statistics
+    (fnofuse.pipeline.layer_op_stats, pipeline.py:369-416) + the CGEMM term
+    (SURVEY.md §8d): 2*op_budget + 6*twiddle_muls + 8*B*kx*ky*H*N."""
+    st = F.layer_op_stats(cfg, "fully_fused")
+    return (2 * st["fft_op_budget"] + 6 * st["fft_twiddle_muls"]
+            + 8 * cfg.batch * cfg.keep_x * cfg.keep_y * cfg.hidden_dim * cfg.output_dim)
+
+
+# ---- CPU reference workers (one process per host core, single-threaded BLAS) ----
+_RW = None
+
+
+def _ref_import(kind):
+    if kind == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import fnofuse
+        return fnofuse
+    from oracle import fnofuse_port
+    return fnofuse_port
+
+
+def _ref_init(kind, cfg1, seed):
+    """Worker initializer: import the CPU implementation, draw this worker's
+    batch element (random_spectral / ComplexMatrix.random, core.py:239-244)."""
+    global _RW
+    F = _ref_import(kind)
+    import numpy as np_
+    if kind == "reference":
+        cfg = F.FnoLayerConfig(**cfg1)
+        rng = np_.random.default_rng(seed + os.getpid())
+        x = F.random_spectral(cfg, rng) if seed >= 0 else None
+        w = F.ComplexMatrix.random(cfg.hidden_dim, cfg.output_dim, rng) if seed >= 0 else None
+    else:
+        from types import SimpleNamespace
+        cfg = SimpleNamespace(**cfg1)
+        x, w = F.random_inputs(cfg, seed + os.getpid()) if seed >= 0 else (None, None)
+    _RW = (kind, F, cfg, x, w)
+
+
+def _ref_step(_i):
+    """One batch element of the workload through the CPU implementation's public API."""
+    kind, F, cfg, x, w = _RW
+    if kind == "reference":
+        y, _led = F.run_layer(cfg, x, w, mode="fully_fused")
+        return float(np.abs(y.data[0, 0, 0, 0]))
+    return float(np.abs(F.run_layer_values(cfg, x, w)[0, 0, 0, 0]))
+
+
+def _ref_run(args):
+    """Run given inputs (parity leg): returns the CPU output values."""
+    x, w = args
+    kind, F, cfg, _, _ = _RW
+    if kind == "reference":
+        y, _led = F.run_layer(cfg, F.SpectralTensor(x), F.ComplexMatrix(w), mode="fully_fused")
+        return np.asarray(y.data)
+    return F.run_layer_values(cfg, x, w)
+
+
+class RefPool:
+    """Batch-sharded CPU execution of the reference's fused layer: `workers`
+    processes (spawned; OPENBLAS_NUM_THREADS=1), one batch element each per
+    step.  kind "reference" = the unmodified fnofuse from baseline/_ref through
+    its public run_layer (pipeline.py:129); "port" = the numpy oracle port
+    (bitwise equal, used only when the install is absent)."""
+
+    def __init__(self, cfg_t, workers, seed=-1):
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        self.kind = "reference" if os.path.isdir(os.path.join(REF_DIR, "fnofuse")) else "port"
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"
+        self.workers = workers
+        cfg1 = dict(cfg_t, batch=1)
+        self.ex = ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn"), initializer=_ref_init,
+                                      initargs=(self.kind, cfg1, seed))
+        self.F = _ref_import(self.kind)
+        self.cfg1 = cfg1
+
+    def step(self):
+        return list(self.ex.map(_ref_step, range(self.workers)))
+
+    def run(self, xs, w):
+        return np.concatenate([y for y in self.ex.map(_ref_run, [(xs[i:i + 1], w) for i in range(len(xs))])],
+                              axis=0)
+
+    def flops(self, batch):
+        if self.kind == "reference":
+            cfg = self.F.FnoLayerConfig(**dict(self.cfg1, batch=batch))
+            return reference_layer_flops(self.F, cfg)
+        from types import SimpleNamespace
+
+        from oracle import fnofuse_port as O
+        return O.layer_flops(SimpleNamespace(**dict(self.cfg1, batch=batch)))
+
+    def close(self):
+        self.ex.shutdown()
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU path (fnofuse.run_layer from
+    baseline/_ref, all host cores, one batch element per process per step) on
+    the same workload/config as our arm.  Never imports the product package."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_2504_11681_b200 as T  # host-side flop counting only (no GPU use)
-    from oracle import fnofuse_port as O
     B, H, N, dx, dy, kx, ky, rk, desc = WORKLOADS[args.workload]
-    workers = len(os.sched_getaffinity(0))
-    sb = max(1, min(B, workers))
-    pool = O.CpuPool(workers)
-    from types import SimpleNamespace
-    # bound the whole run to ~budget_s: calibrate one batch element per worker
-    # on an 8-channel sample, then pick the channel count per step (same
-    # per-channel work as the workload; flops counted for the exact sample)
-    budget_s = float(os.environ.get("TFNO_REF_BUDGET_S", "150"))
-    ch = min(8, H, N)
-    ccal = T.FnoLayerConfig(sb, ch, ch, dx, dy, kx, ky, rk)
-    xc, wc = O.random_inputs(ccal, 1)
-    t0 = time.perf_counter()
-    pool.run(SimpleNamespace(**ccal.__dict__), xc, wc)
-    t_cal = time.perf_counter() - t0
-    per_step = budget_s / max(1, args.steps + args.warmup)
-    scale = max(1.0, per_step / max(t_cal, 1e-3))
-    hs, ns = min(H, max(ch, int(ch * scale))), min(N, max(ch, int(ch * scale)))
-    scfg = T.FnoLayerConfig(sb, hs, ns, dx, dy, kx, ky, rk)
-    x, w = O.random_inputs(scfg, 1234)
-    flops = T.layer_flops(scfg)["flops"]
-    c = SimpleNamespace(**scfg.__dict__)
+    Bl = B // ws if args.scaling == "strong" else B
+    workers = max(1, min(Bl, len(os.sched_getaffinity(0))))
+    cfg_t = dict(batch=1, hidden_dim=H, output_dim=N, dim_x=dx, dim_y=dy, keep_x=kx, keep_y=ky, rank=rk)
+    pool = RefPool(cfg_t, workers, seed=1234)
+    nl = LAYERS.get(args.workload, 1)
+    flops = pool.flops(workers) * nl
     for _ in range(args.warmup):
-        pool.run(c, x, w)
+        for _l in range(nl):
+            pool.step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        pool.run(c, x, w)
+        for _l in range(nl):
+            pool.step()
     dt = (time.perf_counter() - t0) / args.steps
+    kind = pool.kind
     pool.close()
     val = flops / dt / 1e9
-    sample = (f"{sb} batch elements x {hs}->{ns} channels of {args.workload} per step (1 batch element per "
-              f"worker process), numpy oracle port of fnofuse (bitwise equal to the reference)")
-    line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+    src = ("unmodified fnofuse 0.1.0 (baseline/_ref) fnofuse.run_layer(mode='fully_fused')" if kind == "reference"
+           else "numpy oracle port of fnofuse (baseline/_ref absent; bitwise equal to the reference)")
+    sample = (f"{workers} of the {Bl} batch elements of {args.workload} per step x {nl} layer(s), all {H}->{N} "
+              f"channels, 1 batch element per worker process ({workers} processes, OPENBLAS_NUM_THREADS=1): {src}")
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-            "us_per_layer_extrapolated": round(dt * 1e6 * T.layer_flops(T.FnoLayerConfig(B, H, N, dx, dy, kx, ky, rk))["flops"] / flops, 1),
-            "higher_is_better": True, "scaling": "n/a (CPU)", "vs_baseline": None, "dtype": "fp32 (complex64)",
-            "data": "synthetic (seeded N(0,1))",
-            "config": {"workload": desc, "batch_sample": sb, "channels_sample": [hs, ns], "mode": "fully_fused"},
-            "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": workers, "kind": "port",
+            "higher_is_better": True, "scaling": "weak" if args.scaling == "weak" else "strong",
+            "vs_baseline": None, "dtype": "fp32 (complex64 in/out, fp32 arithmetic)",
+            "data": "synthetic (seeded N(0,1) re/im, reference random_spectral)",
+            "config": workload_config(args, Bl, ws),
+            "cpu_baseline": {"value": round(val, 4), "unit": "GFLOP/s", "cores": workers, "kind": kind,
                              "sample": sample},
-            "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(val, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -375,13 +466,8 @@ def run_ours(args):
         "dtype": ("fp32 (complex64 in/out, fp32 arithmetic)" if prec == "fp32" else
                   f"fp32 FFTs + {prec} tcgen05 channel contraction (complex64 in/out)"),
         "data": "synthetic (device-generated N(0,1) re/im, seeded per rank)",
-        "config": {"workload": desc, "batch_per_gpu": B, "global_batch": B * ws, "hidden": H, "out": N,
-                   "dims": [dx, dy], "keep": [kx, ky], "rank": rk, "mode": mode, "precision": prec,
-                   "schedule": sched, "parallelism": f"batch-sharded dp{ws}, no data-path collective",
-                   "l2": (f"inputs larger than L2 ({8 * B * H * dx * dy / 2**30:.1f} GiB per GPU); no flush"
-                          if 8 * B * H * dx * dy > (126 << 20) else
-                          f"inputs ({8 * B * H * dx * dy / 2**20:.1f} MiB) fit in L2: L2-warm timing"),
-                   "launch": "one CUDA graph replay per step" if chain is not None else "eager launches"},
+        "config": workload_config(args, B, ws),
+        "schedule": sched, "launch": "one CUDA graph replay per step" if chain is not None else "eager launches",
         "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": sbytes[dom][1],
@@ -500,24 +586,32 @@ def run_ours(args):
         workers = len(os.sched_getaffinity(0))
         sb = max(1, min(B, workers))
         xs = x[:sb].cpu().numpy()
-        cfg_t = dict(batch=sb, hidden_dim=H, output_dim=N, dim_x=dx, dim_y=dy, keep_x=kx, keep_y=ky, rank=rk)
+        cfg_t = dict(batch=1, hidden_dim=H, output_dim=N, dim_x=dx, dim_y=dy, keep_x=kx, keep_y=ky, rank=rk)
+        pool = RefPool(cfg_t, sb)
         if chain is None:
             wh = w.cpu().numpy()
             ys = y[:sb].cpu().numpy()
-            dt, ref = cpu_reference(cfg_t, xs, wh, workers)
+            t0 = time.perf_counter()
+            ref = pool.run(xs, wh)
+            dt = time.perf_counter() - t0
         else:
             ys = chain.forward(x)[:sb].cpu().numpy()
             dt, ref = 0.0, xs
             for wl in chain.weights:
-                d_, ref = cpu_reference(cfg_t, ref, wl.cpu().numpy(), workers)
-                dt += d_
-        sflops = T.layer_flops(T.FnoLayerConfig(**cfg_t))["flops"] * nlayers
-        result["cpu_baseline"] = {"value": round(sflops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": workers,
-                                  "kind": "port",
+                t0 = time.perf_counter()
+                ref = pool.run(ref, wl.cpu().numpy())
+                dt += time.perf_counter() - t0
+        sflops = pool.flops(sb) * nlayers
+        kind = pool.kind
+        pool.close()
+        src = ("unmodified fnofuse.run_layer from baseline/_ref" if kind == "reference"
+               else "numpy oracle port of fnofuse run_layer")
+        result["cpu_baseline"] = {"value": round(sflops / dt / 1e9, 4), "unit": "GFLOP/s", "cores": sb,
+                                  "kind": kind,
                                   "sample": f"first {sb} batch elements of the timed input, 1 per worker process "
-                                            f"({dt:.1f} s wall), numpy oracle port of fnofuse run_layer"}
+                                            f"({dt:.1f} s wall incl. input pickling), {src}"}
         result["max_rel_error"] = float(T.max_rel_error(ys, ref))
-        result["parity_sample"] = f"batch[0:{sb}] vs CPU oracle (tolerance 1e-5)"
+        result["parity_sample"] = f"batch[0:{sb}] vs the CPU {kind} ({src}); FP32 tolerance 1e-5"
 
     if rank == 0:
         print(json.dumps(result), flush=True)

@@ -44,16 +44,24 @@ def stream_ptr(stream=None) -> int:
 _WS = {}
 
 
-def workspace(nbytes: int, device):
-    """Cached uint8 device workspace of at least nbytes (grown on demand)."""
+def workspace(nbytes: int, device, stream=None):
+    """Cached uint8 device workspace of at least nbytes (grown on demand),
+    one per (device, stream): calls on different streams may run
+    concurrently, so they never share scratch memory.  The buffer is
+    allocated on (and its lifetime tracked against) that stream."""
     t = torch()
-    key = str(device)
+    sp = stream_ptr(stream)
+    key = (str(device), sp)
     buf = _WS.get(key)
     if nbytes == 0:
         return None
     if buf is None or buf.numel() < nbytes:
         _WS.pop(key, None)
-        buf = t.empty(nbytes, dtype=t.uint8, device=device)
+        if stream is not None:
+            with t.cuda.stream(stream):
+                buf = t.empty(nbytes, dtype=t.uint8, device=device)
+        else:
+            buf = t.empty(nbytes, dtype=t.uint8, device=device)
         _WS[key] = buf
     return buf
 

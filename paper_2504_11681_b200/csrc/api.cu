@@ -157,17 +157,9 @@ struct Sched {
   std::string desc;
 };
 
-int num_sms_api() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms_api() { return device_sms(); }  // per device
 
-Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
+Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true) {
   Sched s;
   Geo g = geo_of(c);
   if (mode == TFNO_STAGED) {
@@ -198,7 +190,7 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
   const bool tc_heavy = prec != TFNO_FP32 && g.H * g.N >= 128 * 128;
   const bool f1_full = fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N);
   const int f1_forced = f1_full ? 0 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
-  if (mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1)) {
+  if (allow_f1 && mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1)) {
     s.f1 = true;
     s.f1_cluster = f1_full ? fused1d_cluster((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx) : 1;
     s.f1_split = s.f1_cluster > 1 ? 1 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
@@ -275,11 +267,15 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0) {
 }
 
 // ---------------- staged baseline: cuFFT + cuBLAS ----------------
+// Plans and cuBLAS handles are per (device, stream): a cuFFT plan's work area
+// and a cuBLAS handle's workspace are used by the kernels they enqueue, so two
+// streams running the staged layer concurrently (HostPipeline) must not share them.
 struct BaselineCtx {
-  cublasHandle_t blas = nullptr;
-  std::map<std::tuple<int, int, int, int64_t>, cufftHandle> plans;
+  std::map<cudaStream_t, cublasHandle_t> blas;
+  std::map<std::tuple<int, int, int, int64_t, cudaStream_t>, cufftHandle> plans;
 };
 BaselineCtx g_base[64];
+std::mutex g_base_mu[64];  // guards the per-device caches (enqueue only)
 
 int staged_chunk(const Geo& g) {
   // batch chunk so that the full forward spectrum of a chunk is <= 8 GiB
@@ -294,8 +290,8 @@ size_t staged_ws(const Geo& g) {
   return (size_t)(bc * g.H * g.dx * g.dy + g.B * g.H * g.kx * g.ky + g.B * g.N * g.kx * g.ky) * 8;
 }
 
-int get_plan(int dev, int rank, int dx, int dy, int64_t batch, cufftHandle* out) {
-  auto key = std::make_tuple(rank, dx, dy, batch);
+int get_plan(int dev, int rank, int dx, int dy, int64_t batch, cudaStream_t st, cufftHandle* out) {
+  auto key = std::make_tuple(rank, dx, dy, batch, st);
   auto& ctx = g_base[dev];
   auto it = ctx.plans.find(key);
   if (it != ctx.plans.end()) {
@@ -329,11 +325,16 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   if (ws_bytes < staged_ws(g)) return TFNO_EWORKSPACE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TFNO_ECUDA;
-  std::lock_guard<std::mutex> lk(g_mu);
+  if (dev < 0 || dev >= 64) return TFNO_ECUDA;
+  std::lock_guard<std::mutex> lk(g_base_mu[dev]);
   auto& ctx = g_base[dev];
-  if (!ctx.blas) {
-    if (cublasCreate(&ctx.blas) != CUBLAS_STATUS_SUCCESS) return TFNO_ECUBLAS;
-    cublasSetMathMode(ctx.blas, CUBLAS_DEFAULT_MATH);  // true FP32, no TF32
+  cublasHandle_t& blas = ctx.blas[st];
+  if (!blas) {
+    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) {
+      ctx.blas.erase(st);
+      return TFNO_ECUBLAS;
+    }
+    cublasSetMathMode(blas, CUBLAS_DEFAULT_MATH);  // true FP32, no TF32
   }
   const int64_t bc = staged_chunk(g);
   float2* full = ws;
@@ -345,7 +346,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   for (int64_t b0 = 0; b0 < g.B; b0 += bc) {
     int64_t nb = (g.B - b0 < bc) ? g.B - b0 : bc;
     cufftHandle p;
-    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.H, &p);
+    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.H, st, &p);
     if (e) return e;
     cufftSetStream(p, st);
     if (cufftExecC2C(p, (cufftComplex*)(x + b0 * g.H * plane), (cufftComplex*)full, CUFFT_FORWARD) !=
@@ -357,9 +358,9 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   }
   stage_mark(st);
   // CGEMM over the channel axis, 1/(dx*dy) folded into alpha
-  cublasSetStream(ctx.blas, st);
+  cublasSetStream(blas, st);
   cuComplex alpha = make_cuComplex((float)(1.0 / (double)(g.dx * g.dy)), 0.f), beta = make_cuComplex(0.f, 0.f);
-  cublasStatus_t bs = cublasCgemmStridedBatched(ctx.blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)modes, (int)g.N, (int)g.H,
+  cublasStatus_t bs = cublasCgemmStridedBatched(blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)modes, (int)g.N, (int)g.H,
                                                 &alpha, (const cuComplex*)A, (int)modes, g.H * modes,
                                                 (const cuComplex*)w, (int)g.N, 0, &beta, (cuComplex*)Cm,
                                                 (int)modes, g.N * modes, (int)g.B);
@@ -374,7 +375,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   for (int64_t b0 = 0; b0 < g.B; b0 += obc) {
     int64_t nb = (g.B - b0 < obc) ? g.B - b0 : obc;
     cufftHandle p;
-    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.N, &p);
+    int e = get_plan(dev, g.rank, (int)g.dx, (int)g.dy, nb * g.N, st, &p);
     if (e) return e;
     cufftSetStream(p, st);
     cufftComplex* yy = (cufftComplex*)(y + b0 * g.N * plane);
@@ -638,6 +639,22 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   const size_t wimg_need = wimg_bytes_for(c, mode, prec);
   Geo g = geo_of(c);
   Sched s = make_sched(c, mode, prec);
+  if (s.f1 && ((((uintptr_t)x | (uintptr_t)w | (uintptr_t)y) & 15) != 0 || (g.rank == 2 && (g.dy * 8) % 16))) {
+    // the fused 1D kernel moves rows with 16-byte TMA bulk copies: a valid but
+    // misaligned view (e.g. w_all[i] with odd H*N) takes the next schedule
+    Sched s2 = make_sched(c, mode, prec, false);
+    size_t need2 = 0;
+    {
+      if (s2.need_s1) need2 += g.B * g.H * g.kx * g.dy;
+      if (s2.need_mid) need2 += g.B * g.N * g.kx * g.dy;
+      if (s2.need_A) need2 += g.B * g.H * g.kx * g.ky;
+      if (s2.need_C) need2 += g.B * g.N * g.kx * g.ky;
+      need2 *= sizeof(float2);
+    }
+    if (ws_bytes < need2 || (need2 && !ws)) return TFNO_EUNSUPPORTED;
+    s = s2;
+  }
+  if (s.plane2d && ((((uintptr_t)x | (uintptr_t)y) & 15) != 0)) return TFNO_EUNSUPPORTED;  // TMA rows
   if (s.staged) return staged_forward(c, x, w, y, ws, ws_bytes, st);
   int err = 0;
   const float2* tw = twiddle_table(err);

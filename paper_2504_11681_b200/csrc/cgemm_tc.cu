@@ -689,12 +689,7 @@ static cudaError_t launch_tc_t(const GemmArgs& g, cudaStream_t s) {
   cudaError_t e =
       cudaFuncSetAttribute(cgemm_tc_kernel<NP, PASSES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * ((g.N + NP / 2 - 1) / (NP / 2)) * g.batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
   cgemm_tc_kernel<NP, PASSES><<<grid, 128, smem, s>>>(g);

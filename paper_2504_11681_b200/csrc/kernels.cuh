@@ -97,5 +97,6 @@ cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int s
                                 float scale, cudaStream_t s);
 
 extern thread_local long long g_launches;  // our kernels launched by this thread
+int device_sms();  // SM count of the current device (cached per device)
 
 }  // namespace tfno

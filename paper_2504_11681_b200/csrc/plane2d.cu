@@ -508,16 +508,7 @@ static int plane_variant() {
   return env >= 0 ? env : plane_variant_default<G>();
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms() { return device_sms(); }
 
 template <class G, int S, bool NAT, bool DLD>
 static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {

@@ -20,13 +20,7 @@ namespace tfno {
 namespace {
 
 inline int grid_for(int64_t work) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = tfno::device_sms();
   int64_t g = (work + 255) / 256;
   const int64_t cap = (int64_t)sms * 8;
   return (int)(g < 1 ? 1 : (g > cap ? cap : g));

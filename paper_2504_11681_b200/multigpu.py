@@ -76,15 +76,26 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
 
 
 # ---------------------------------------------------------------- hidden split
+def _on(stream):
+    """Run a helper with `stream` as torch's current stream, so every temporary
+    is allocated on (and recycled against) the stream its kernels run on, and
+    NCCL collectives issued inside are ordered after those kernels."""
+    import contextlib
+    t = _device.torch()
+    return t.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
 def spectrum_forward(cfg: FnoLayerConfig, x, stream=None):
     """modes[B][H][kx][ky] (natural order) = first-keep DFT of every plane (GPU)."""
     t = _device.torch()
     c = cfg_struct(cfg)
-    modes = t.empty((cfg.batch, cfg.hidden_dim, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x.device)
-    nb = int(lib().tfno_spectrum_workspace_bytes(ctypes.byref(c), -1))
-    ws = t.empty(max(nb, 1), dtype=t.uint8, device=x.device)
-    check(lib().tfno_spectrum_forward(ctypes.byref(c), x.data_ptr(), modes.data_ptr(), ws.data_ptr(), nb,
-                                      _device.stream_ptr(stream)), "tfno_spectrum_forward")
+    with _on(stream):
+        modes = t.empty((cfg.batch, cfg.hidden_dim, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x.device)
+        nb = int(lib().tfno_spectrum_workspace_bytes(ctypes.byref(c), -1))
+        ws = _device.workspace(nb, x.device, stream)  # cached per (device, stream): no per-call allocation
+        check(lib().tfno_spectrum_forward(ctypes.byref(c), x.data_ptr(), modes.data_ptr(),
+                                          ws.data_ptr() if ws is not None else None, nb,
+                                          _device.stream_ptr(stream)), "tfno_spectrum_forward")
     return modes
 
 
@@ -92,11 +103,13 @@ def spectrum_inverse(cfg: FnoLayerConfig, modes, planes_shape, scale: float = 1.
     """y[planes] = scale * zero-padded normalised inverse of natural-order modes (GPU)."""
     t = _device.torch()
     c = cfg_struct(cfg)
-    y = t.empty(tuple(planes_shape) + (cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=modes.device)
-    nb = int(lib().tfno_spectrum_workspace_bytes(ctypes.byref(c), 1))
-    ws = t.empty(max(nb, 1), dtype=t.uint8, device=modes.device)
-    check(lib().tfno_spectrum_inverse(ctypes.byref(c), modes.data_ptr(), y.data_ptr(), float(scale),
-                                      ws.data_ptr(), nb, _device.stream_ptr(stream)), "tfno_spectrum_inverse")
+    with _on(stream):
+        y = t.empty(tuple(planes_shape) + (cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=modes.device)
+        nb = int(lib().tfno_spectrum_workspace_bytes(ctypes.byref(c), 1))
+        ws = _device.workspace(nb, modes.device, stream)
+        check(lib().tfno_spectrum_inverse(ctypes.byref(c), modes.data_ptr(), y.data_ptr(), float(scale),
+                                          ws.data_ptr() if ws is not None else None, nb,
+                                          _device.stream_ptr(stream)), "tfno_spectrum_inverse")
     return y
 
 
@@ -109,19 +122,20 @@ def hidden_split_partial(cfg: FnoLayerConfig, x_shard, w_shard, channel_major: b
     t = _device.torch()
     lc = FnoLayerConfig(cfg.batch, x_shard.shape[1], cfg.output_dim, cfg.dim_x, cfg.dim_y,
                         cfg.keep_x, cfg.keep_y, cfg.rank)
-    A = spectrum_forward(lc, x_shard, stream)
-    B, Hr, N = cfg.batch, x_shard.shape[1], cfg.output_dim
-    MQ = cfg.keep_x * cfg.keep_y
-    w = w_shard.contiguous()
-    if channel_major:
-        C = t.empty((N, B, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x_shard.device)
-        c_ns, c_bs = B * MQ, MQ
-    else:
-        C = t.empty((B, N, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x_shard.device)
-        c_ns, c_bs = MQ, N * MQ
-    rc = lib().tfno_cgemm(MQ, N, Hr, B, A.data_ptr(), 1, MQ, Hr * MQ, w.data_ptr(), N, 1, 0,
-                          C.data_ptr(), 1, c_ns, c_bs, 1.0, _device.stream_ptr(stream))
-    check(rc, "tfno_cgemm")
+    with _on(stream):
+        A = spectrum_forward(lc, x_shard, stream)
+        B, Hr, N = cfg.batch, x_shard.shape[1], cfg.output_dim
+        MQ = cfg.keep_x * cfg.keep_y
+        w = w_shard.contiguous()
+        if channel_major:
+            C = t.empty((N, B, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x_shard.device)
+            c_ns, c_bs = B * MQ, MQ
+        else:
+            C = t.empty((B, N, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x_shard.device)
+            c_ns, c_bs = MQ, N * MQ
+        rc = lib().tfno_cgemm(MQ, N, Hr, B, A.data_ptr(), 1, MQ, Hr * MQ, w.data_ptr(), N, 1, 0,
+                              C.data_ptr(), 1, c_ns, c_bs, 1.0, _device.stream_ptr(stream))
+        check(rc, "tfno_cgemm")
     return C
 
 
@@ -159,11 +173,14 @@ def hidden_split_forward(cfg: FnoLayerConfig, x_shard, w_shard, how: str = "all_
     import torch.distributed as dist
     world = dist.get_world_size(group)
     cm = how == "reduce_scatter"
-    C = hidden_split_partial(cfg, x_shard, w_shard, channel_major=cm, stream=stream)
-    C = reduce_partials(C, how, group)
-    if cm:
-        nr = cfg.output_dim // world
-        pc = FnoLayerConfig(1, 1, nr * cfg.batch, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
-        return spectrum_inverse(pc, C, (nr, cfg.batch), 1.0, stream)
-    oc = FnoLayerConfig(cfg.batch, 1, cfg.output_dim, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
-    return spectrum_inverse(oc, C, (cfg.batch, cfg.output_dim), 1.0, stream)
+    # one stream for partial -> NCCL reduce -> inverse: the collective (enqueued
+    # on torch's current stream) is ordered after the partial CGEMM
+    with _on(stream):
+        C = hidden_split_partial(cfg, x_shard, w_shard, channel_major=cm, stream=stream)
+        C = reduce_partials(C, how, group)
+        if cm:
+            nr = cfg.output_dim // world
+            pc = FnoLayerConfig(1, 1, nr * cfg.batch, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
+            return spectrum_inverse(pc, C, (nr, cfg.batch), 1.0, stream)
+        oc = FnoLayerConfig(cfg.batch, 1, cfg.output_dim, cfg.dim_x, cfg.dim_y, cfg.keep_x, cfg.keep_y, cfg.rank)
+        return spectrum_inverse(oc, C, (cfg.batch, cfg.output_dim), 1.0, stream)

@@ -220,6 +220,14 @@ def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILE
         raise FnofuseError("run_layer_device needs CUDA tensors (no CPU fallback)")
     x = x if (x.dtype == t.complex64 and x.is_contiguous()) else x.to(t.complex64).contiguous()
     w = w if (w.dtype == t.complex64 and w.is_contiguous()) else w.to(t.complex64).contiguous()
+    # the kernels move rows with 16-byte TMA bulk copies: odd-element views get an aligned copy
+    if x.data_ptr() % 16:
+        x = x.clone()
+    if w.data_ptr() % 16:
+        w = w.clone()
+    user_out = None
+    if out is not None and out.data_ptr() % 16:
+        user_out, out = out, None
     if out is None:
         out = t.empty((cfg.batch, cfg.output_dim, cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=dev)
     c = cfg_struct(cfg)
@@ -228,13 +236,18 @@ def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILE
     if workspace is not None and workspace.numel() >= nbytes:
         ws = workspace if nbytes else None
     else:
-        ws = _device.workspace(nbytes, dev)
-        if ws is not None and stream is not None:
-            ws.record_stream(stream)  # a later regrowth must not recycle it under this stream's kernels
+        ws = _device.workspace(nbytes, dev, stream)  # per (device, stream): no sharing across streams
     rc = lib().tfno_layer_forward(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                   ws.data_ptr() if ws is not None else None, nbytes,
                                   _device.stream_ptr(stream))
     check(rc, "tfno_layer_forward")
+    if user_out is not None:
+        if stream is not None:
+            with t.cuda.stream(stream):
+                user_out.copy_(out)
+        else:
+            user_out.copy_(out)
+        return user_out
     return out
 
 

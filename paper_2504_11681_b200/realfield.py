@@ -45,20 +45,22 @@ def real_spectral(cfg: FnoLayerConfig, x, w, stream=None):
         raise ShapeMismatch(f"x must be float32 {(B, H, cfg.dim_x, cfg.dim_y)}, got {x.dtype} {tuple(x.shape)}")
     if tuple(w.shape) != (H, N):
         raise ShapeMismatch(f"w shape {tuple(w.shape)} != {(H, N)}")
-    x = x.contiguous()
-    w = w.to(t.complex64).contiguous()
     sp = _device.stream_ptr(stream)
-    xc = t.empty(x.shape, dtype=t.complex64, device=x.device)
-    check(lib().tfno_real_to_complex(x.data_ptr(), xc.data_ptr(), x.numel(), sp), "tfno_real_to_complex")
-    A = spectrum_forward(cfg, xc, stream)                                   # [B,H,kx,ky]
-    del xc
-    MQ = cfg.keep_x * cfg.keep_y
-    check(lib().tfno_half_spectrum_weight(A.data_ptr(), B * H * cfg.keep_x, cfg.keep_y, cfg.dim_y, sp),
-          "tfno_half_spectrum_weight")
-    C = t.empty((B, N, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x.device)
-    check(lib().tfno_cgemm(MQ, N, H, B, A.data_ptr(), 1, MQ, H * MQ, w.data_ptr(), N, 1, 0,
-                           C.data_ptr(), 1, MQ, N * MQ, 1.0, sp), "tfno_cgemm")
-    return spectrum_inverse(cfg, C, (B, N), scale=1.0, stream=stream)
+    # temporaries allocated on the stream the kernels run on (no cross-stream reuse)
+    with (t.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
+        x = x.contiguous()
+        w = w.to(t.complex64).contiguous()
+        xc = t.empty(x.shape, dtype=t.complex64, device=x.device)
+        check(lib().tfno_real_to_complex(x.data_ptr(), xc.data_ptr(), x.numel(), sp), "tfno_real_to_complex")
+        A = spectrum_forward(cfg, xc, stream)                                   # [B,H,kx,ky]
+        del xc
+        MQ = cfg.keep_x * cfg.keep_y
+        check(lib().tfno_half_spectrum_weight(A.data_ptr(), B * H * cfg.keep_x, cfg.keep_y, cfg.dim_y, sp),
+              "tfno_half_spectrum_weight")
+        C = t.empty((B, N, cfg.keep_x, cfg.keep_y), dtype=t.complex64, device=x.device)
+        check(lib().tfno_cgemm(MQ, N, H, B, A.data_ptr(), 1, MQ, H * MQ, w.data_ptr(), N, 1, 0,
+                               C.data_ptr(), 1, MQ, N * MQ, 1.0, sp), "tfno_cgemm")
+        return spectrum_inverse(cfg, C, (B, N), scale=1.0, stream=stream)
 
 
 def fno_block(cfg: FnoLayerConfig, x, w, bypass_w=None, bias=None, activation=None, out=None, stream=None):

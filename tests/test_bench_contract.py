@@ -49,3 +49,19 @@ def test_reference_arm_under_torchrun_world2():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_reference_arm_never_loads_the_product():
+    """The reference arm times the unmodified reference (or the port) and must not
+    import the product package or map libturbofno.so (void ratio)."""
+    code = ("import sys, json; sys.argv=['bench.py','--impl','reference','--workload','C1','--steps','1',"
+            "'--warmup','3']; import bench; bench.main(); "
+            "assert not [m for m in sys.modules if m.startswith('paper_2504_11681_b200')]; "
+            "maps=open('/proc/self/maps').read(); assert 'libturbofno' not in maps; print('CLEAN')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "CLEAN" in r.stdout
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "fnofuse")):
+        assert d["cpu_baseline"]["kind"] == "reference"
+    assert d["config"]["hidden"] == 64 and d["config"]["out"] == 64

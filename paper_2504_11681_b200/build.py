@@ -22,6 +22,8 @@ BUILD_DIR = os.path.join(HERE, "_build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart", "shared",
               "-Xptxas", "-v"] + ARCH
+# (source, extra nvcc flags, object name): plane_g.cu is built once per row length
+PLANE_G = [("plane_g.cu", ["-DPLANE_G_DY=%d" % d], "plane_g_%d.cu.o" % d) for d in (64, 128, 256, 512, 1024)]
 SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "warpfft_fwd.cu", "fused1d.cu", "realfield.cu", "api.cu", "plan.cpp"]
 
 
@@ -45,13 +47,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD_DIR, exist_ok=True)
     nvcc = _nvcc()
 
-    def compile_one(src):
-        obj = os.path.join(BUILD_DIR, src + ".o")
+    def compile_one(item):
+        src, extra, oname = item if isinstance(item, tuple) else (item, [], item + ".o")
+        obj = os.path.join(BUILD_DIR, oname)
         path = os.path.join(CSRC, src)
         if src.endswith(".cpp"):
             cmd = [nvcc, "-O3", "-std=c++17", "-Wno-deprecated-gpu-targets", "-Xcompiler", "-fPIC", "-c", path, "-o", obj]
         else:
-            cmd = [nvcc] + NVCC_FLAGS + ["-I", INCLUDE, "-c", path, "-o", obj]
+            cmd = [nvcc] + NVCC_FLAGS + extra + ["-I", INCLUDE, "-c", path, "-o", obj]
             # A/B hook: TFNO_SCALAR_FILES=a.cu,b.cu builds those files with the scalar complex primitives
             if src in os.environ.get("TFNO_SCALAR_FILES", "").split(","):
                 cmd.insert(1, "-DTFNO_SCALAR_COMPLEX")
@@ -63,14 +66,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
         if verbose:
             sys.stderr.write(res.stderr)
-        with open(os.path.join(BUILD_DIR, src + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(BUILD_DIR, oname[:-2] + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
         return obj
 
     # translation units are independent: compile them in parallel
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    items = PLANE_G + SOURCES
+    with ThreadPoolExecutor(max_workers=min(len(items), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, items))
     tmp = OUT + ".tmp"
     cmd = [nvcc, "-shared", "--cudart", "shared"] + ARCH + ["-o", tmp] + objs + [
         "-L/usr/local/cuda/lib64", "-lcufft", "-lcublas", "-lcudart",

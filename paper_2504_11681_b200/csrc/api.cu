@@ -403,8 +403,9 @@ size_t base_ws_bytes(const tfno_cfg* c, int mode, int prec) {  // intermediates 
   size_t e = 0;
   if (s.need_s1) e += g.B * g.H * g.kx * g.dy;
   if (s.need_mid) e += g.B * g.N * g.kx * g.dy;
-  if (s.need_A) e += g.B * g.H * g.kx * g.ky;
-  if (s.need_C) e += g.B * g.N * g.kx * g.ky;
+  const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;  // generic plane kernels: KP^2 padded modes
+  if (s.need_A) e += g.B * g.H * mq;
+  if (s.need_C) e += g.B * g.N * mq;
   return e * sizeof(float2);
 }
 
@@ -561,7 +562,7 @@ int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, cons
 
 size_t tfno_spectrum_workspace_bytes(const tfno_cfg* c, int direction) {
   if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
-  if (c->rank != 2 || plane2d_supported(c)) return 0;
+  if (c->rank != 2 || plane2d_spectrum_ok(c)) return 0;
   Geo g = geo_of(c);
   return (size_t)((direction < 0 ? g.H : g.N) * g.B * g.kx * g.dy) * sizeof(float2);
 }
@@ -577,7 +578,7 @@ int tfno_spectrum_forward(const tfno_cfg* c, const void* xv, void* modes, void* 
   Geo g = geo_of(c);
   const float2* x = (const float2*)xv;
   float2* A = (float2*)modes;
-  if (plane2d_supported(c)) return cuda_status(launch_plane2d_fwd(c, x, A, tw, st));
+  if (plane2d_spectrum_ok(c)) return cuda_status(launch_plane2d_fwd(c, x, A, tw, st));
   const float2* src = x;
   if (g.rank == 2) {
     float2* s1 = (float2*)wsv;
@@ -604,7 +605,7 @@ int tfno_spectrum_inverse(const tfno_cfg* c, const void* modes, void* yv, float 
   Geo g = geo_of(c);
   const float2* Cm = (const float2*)modes;
   float2* y = (float2*)yv;
-  if (plane2d_supported(c))
+  if (plane2d_spectrum_ok(c))
     return cuda_status(launch_plane2d_inv(c, Cm, y, (float)(scale / ((double)g.dx * g.dy)), tw, st));
   float2* dst = g.rank == 2 ? (float2*)wsv : y;
   float sy = (float)(1.0 / (double)g.dy) * (g.rank == 2 ? 1.0f : scale);
@@ -668,8 +669,9 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   float2* Cm = nullptr;
   if (s.need_s1) { s1 = p; p += g.B * g.H * g.kx * g.dy; }
   if (s.need_mid) { mid = p; p += g.B * g.N * g.kx * g.dy; }
-  if (s.need_A) { A = p; p += g.B * g.H * g.kx * g.ky; }
-  if (s.need_C) { Cm = p; p += g.B * g.N * g.kx * g.ky; }
+  const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;
+  if (s.need_A) { A = p; p += g.B * g.H * mq; }
+  if (s.need_C) { Cm = p; p += g.B * g.N * mq; }
   void* wimg = (wimg_need && ws_bytes >= need + wimg_need) ? (void*)p : nullptr;
 
   stage_begin(st);

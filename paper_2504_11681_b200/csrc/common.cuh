@@ -157,6 +157,152 @@ __device__ __forceinline__ void dft8(float2* v) {
   v[7] = csub(e3, t3);
 }
 
+// 16-point DFT, natural order in and out: n = n1 + 4 n2, k = k1 + 4 k2 --
+// four radix-4 DFTs over n2, twiddles w16^{n1 k1}, four radix-4 DFTs over n1
+// (the final 4x4 transpose is register renaming).
+template <int DIR>
+__device__ __forceinline__ void dft16(float2* v) {
+  const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f, r2 = 0.70710678118654752440f;
+  const float d = (float)DIR;
+#pragma unroll
+  for (int n1 = 0; n1 < 4; ++n1) dft4<DIR>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
+  // Y[n1][k1] now at v[n1 + 4 k1]; twiddle w16^{n1 k1}
+  v[1 + 4] = cmul(v[1 + 4], make_float2(c1, d * s1));     // w^1
+  v[1 + 8] = cmul(v[1 + 8], make_float2(r2, d * r2));     // w^2
+  v[1 + 12] = cmul(v[1 + 12], make_float2(s1, d * c1));   // w^3
+  v[2 + 4] = cmul(v[2 + 4], make_float2(r2, d * r2));     // w^2
+  v[2 + 8] = mul_dir_i<DIR>(v[2 + 8]);                    // w^4 = DIR i
+  v[2 + 12] = cmul(v[2 + 12], make_float2(-r2, d * r2));  // w^6
+  v[3 + 4] = cmul(v[3 + 4], make_float2(s1, d * c1));     // w^3
+  v[3 + 8] = cmul(v[3 + 8], make_float2(-r2, d * r2));    // w^6
+  v[3 + 12] = cmul(v[3 + 12], make_float2(-c1, -d * s1)); // w^9
+  float2 o[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    float2 y0 = v[0 + 4 * k1], y1 = v[1 + 4 * k1], y2 = v[2 + 4 * k1], y3 = v[3 + 4 * k1];
+    dft4<DIR>(y0, y1, y2, y3);
+    o[k1] = y0;
+    o[k1 + 4] = y1;
+    o[k1 + 8] = y2;
+    o[k1 + 12] = y3;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+
+// ---- input-pruned DFTs: inputs n >= NIN are known zeros (no adds of zeros;
+// unused outputs are removed by the compiler anyway)
+template <int DIR, int NIN>
+__device__ __forceinline__ void dft4_in(float2& x0, float2& x1, float2& x2, float2& x3) {
+  if constexpr (NIN >= 4) {
+    dft4<DIR>(x0, x1, x2, x3);
+  } else if constexpr (NIN == 3) {
+    const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
+    x0 = cadd(t0, x1);
+    x2 = csub(t0, x1);
+    const float2 a = cadd_dir_i<DIR>(t1, x1), b = csub_dir_i<DIR>(t1, x1);
+    x1 = a;
+    x3 = b;
+  } else if constexpr (NIN == 2) {
+    const float2 a = x0, b = x1;
+    x0 = cadd(a, b);
+    x2 = csub(a, b);
+    x1 = cadd_dir_i<DIR>(a, b);
+    x3 = csub_dir_i<DIR>(a, b);
+  } else if constexpr (NIN == 1) {
+    x1 = x0;
+    x2 = x0;
+    x3 = x0;
+  } else {
+    x0 = x1 = x2 = x3 = make_float2(0.f, 0.f);
+  }
+}
+
+template <int DIR, int NIN>
+__device__ __forceinline__ void dft8_in(float2* v) {
+  if constexpr (NIN >= 8) {
+    dft8<DIR>(v);
+  } else {
+    constexpr int NE = (NIN + 1) / 2, NO = NIN / 2;
+    const float r = 0.70710678118654752440f;
+    float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4_in<DIR, NE>(e0, e1, e2, e3);
+    if constexpr (NO == 0) {
+      v[0] = v[4] = e0;
+      v[1] = v[5] = e1;
+      v[2] = v[6] = e2;
+      v[3] = v[7] = e3;
+    } else {
+      dft4_in<DIR, NO>(o0, o1, o2, o3);
+      const float2 t1 = cscale(cadd_dir_i<DIR>(o1, o1), r);
+      const float2 t3 = cscale(csub(mul_dir_i<DIR>(o3), o3), r);
+      v[0] = cadd(e0, o0);
+      v[4] = csub(e0, o0);
+      v[1] = cadd(e1, t1);
+      v[5] = csub(e1, t1);
+      v[2] = cadd_dir_i<DIR>(e2, o2);
+      v[6] = csub_dir_i<DIR>(e2, o2);
+      v[3] = cadd(e3, t3);
+      v[7] = csub(e3, t3);
+    }
+  }
+}
+
+template <int DIR, int NIN>
+__device__ __forceinline__ void dft16_in(float2* v) {
+  if constexpr (NIN >= 16) {
+    dft16<DIR>(v);
+  } else {
+    const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f, r2 = 0.70710678118654752440f;
+    const float d = (float)DIR;
+    // step 1: radix 4 over n2 for each n1 (inputs n1 + 4 n2 < NIN)
+    dft4_in<DIR, (NIN + 3) / 4>(v[0], v[4], v[8], v[12]);
+    dft4_in<DIR, (NIN + 2) / 4>(v[1], v[5], v[9], v[13]);
+    dft4_in<DIR, (NIN + 1) / 4>(v[2], v[6], v[10], v[14]);
+    dft4_in<DIR, NIN / 4>(v[3], v[7], v[11], v[15]);
+    constexpr int N1 = NIN < 4 ? NIN : 4;  // nonzero n1 rows
+    if constexpr (N1 > 1) {
+      v[1 + 4] = cmul(v[1 + 4], make_float2(c1, d * s1));
+      v[1 + 8] = cmul(v[1 + 8], make_float2(r2, d * r2));
+      v[1 + 12] = cmul(v[1 + 12], make_float2(s1, d * c1));
+    }
+    if constexpr (N1 > 2) {
+      v[2 + 4] = cmul(v[2 + 4], make_float2(r2, d * r2));
+      v[2 + 8] = mul_dir_i<DIR>(v[2 + 8]);
+      v[2 + 12] = cmul(v[2 + 12], make_float2(-r2, d * r2));
+    }
+    if constexpr (N1 > 3) {
+      v[3 + 4] = cmul(v[3 + 4], make_float2(s1, d * c1));
+      v[3 + 8] = cmul(v[3 + 8], make_float2(-r2, d * r2));
+      v[3 + 12] = cmul(v[3 + 12], make_float2(-c1, -d * s1));
+    }
+    float2 o[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      float2 y0 = v[0 + 4 * k1], y1 = v[1 + 4 * k1], y2 = v[2 + 4 * k1], y3 = v[3 + 4 * k1];
+      dft4_in<DIR, N1>(y0, y1, y2, y3);
+      o[k1] = y0;
+      o[k1 + 4] = y1;
+      o[k1 + 8] = y2;
+      o[k1 + 12] = y3;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = o[k];
+  }
+}
+
+// V-point DFT with the inputs n >= NIN known to be zero
+template <int V, int DIR, int NIN>
+__device__ __forceinline__ void dft_in(float2* v) {
+  if constexpr (V == 16)
+    dft16_in<DIR, NIN>(v);
+  else {
+    static_assert(V == 8, "dft_in: V in {8, 16}");
+    dft8_in<DIR, NIN>(v);
+  }
+}
+
 template <int R, int DIR>
 __device__ __forceinline__ void dft(float2* v) {
   if constexpr (R == 2) {
@@ -165,6 +311,8 @@ __device__ __forceinline__ void dft(float2* v) {
     dft4<DIR>(v[0], v[1], v[2], v[3]);
   } else if constexpr (R == 8) {
     dft8<DIR>(v);
+  } else if constexpr (R == 16) {
+    dft16<DIR>(v);
   } else if constexpr (R == 1) {
   }
 }

@@ -564,24 +564,6 @@ static cudaError_t launch_inv(const float2* Cm, float2* y, int64_t planes, const
              : launch_inv_v<G, SO, false, false>(Cm, y, planes, tw, scale, st);
 }
 
-template <class G, int S, int SO, class GF = G, class GI = G>
-static cudaError_t run_pair(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A, float2* Cm,
-                            const float2* tw, int prec, void* wimg, cudaStream_t st, void (*mark)(cudaStream_t)) {
-  const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
-  cudaError_t e = launch_fwd<GF, S>(x, A, B * H, tw, false, st);
-  if (e != cudaSuccess) return e;
-  if (mark) mark(st);
-  // channel mixing over modes, 1/(dx*dy) folded into alpha
-  const int64_t MQ = (int64_t)G::KX * G::KY;
-  GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ, (float)(1.0 / ((double)G::DX * G::NY))};
-  ga.wimg = wimg;
-  if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e;
-  if (mark) mark(st);
-  if ((e = launch_inv<GI, SO>(Cm, y, B * N, tw, 1.0f, false, st)) != cudaSuccess) return e;
-  if (mark) mark(st);
-  return cudaSuccess;
-}
-
 using G512 = PlaneGeo<512, 64, 512, 64, 512>;
 // forward of the 512 geometry: 4 teams x 2 interleaved rows (ILP against the
 // shared-memory latency that bounds the packed-math forward), same smem
@@ -620,52 +602,140 @@ static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
 static_assert(fwd_smem<G512f>(3) <= 227 * 1024, "smem");
 static_assert(inv_smem<G512>(3) <= 227 * 1024, "smem");
 
-bool plane2d_supported(const tfno_cfg* c) {
+// the four hand-tuned geometries (C3 / C4 / C5 plane shapes + 128^2 keep 16)
+static bool plane2d_tuned(const tfno_cfg* c) {
   if (c->rank != 2 || c->batch * (int64_t)c->hidden_dim > (1LL << 40)) return false;
   const int dx = c->dim_x, dy = c->dim_y, kx = c->keep_x, ky = c->keep_y;
   return (dx == 512 && dy == 512 && kx == 64 && ky == 64) || (dx == 256 && dy == 256 && kx == 32 && ky == 32) ||
          (dx == 256 && dy == 256 && kx == 16 && ky == 16) || (dx == 128 && dy == 128 && kx == 16 && ky == 16);
 }
 
+// generic per-plane kernels (plane_g.cuh): padded keep KP (power of two, 8..128)
+int plane_g_kp(const tfno_cfg* c) {
+  if (c->rank != 2 || (int64_t)c->batch * c->hidden_dim > (1LL << 40) ||
+      (int64_t)c->batch * c->output_dim > (1LL << 40))
+    return 0;
+  const int dx = c->dim_x, dy = c->dim_y;
+  if (dy < 64 || dy > 1024 || (dy & (dy - 1)) || dx > 1024 || (dx & (dx - 1))) return 0;
+  const int k = c->keep_x > c->keep_y ? c->keep_x : c->keep_y;
+  int kp = 8;
+  while (kp < k) kp <<= 1;
+  if (kp > 128 || kp > dy || kp > dx) return 0;
+  return kp;
+}
+
+static int plane_generic_env() {  // TFNO_PLANE_GENERIC=0..3 (bit 0 forward, bit 1 inverse) for A/B
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFNO_PLANE_GENERIC");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+static int plane_mix(const tfno_cfg* c);
+
+bool plane2d_supported(const tfno_cfg* c) { return plane2d_tuned(c) || plane_g_kp(c) > 0; }
+
+int64_t plane2d_modes(const tfno_cfg* c) {
+  if (plane2d_tuned(c)) return (int64_t)c->keep_x * c->keep_y;  // == KP^2 there
+  const int kp = plane_g_kp(c);
+  return (int64_t)kp * kp;
+}
+
+bool plane2d_spectrum_ok(const tfno_cfg* c) {
+  if (plane2d_tuned(c)) return true;
+  const int kp = plane_g_kp(c);
+  return kp > 0 && c->keep_x == kp && c->keep_y == kp;
+}
+
+cudaError_t plane_g_run_64(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
+cudaError_t plane_g_run_128(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
+cudaError_t plane_g_run_256(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
+cudaError_t plane_g_run_512(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
+cudaError_t plane_g_run_1024(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
+
+static cudaError_t plane_g_run(const tfno_cfg* c, int dir, const float2* in, float2* out, int64_t planes,
+                               const float2* tw, float scale, cudaStream_t st) {
+  const int kp = plane_g_kp(c);
+  if (!kp) return cudaErrorNotSupported;
+  const int dx = c->dim_x, kx = c->keep_x, ky = c->keep_y;
+  switch (c->dim_y) {
+    case 64: return plane_g_run_64(kp, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+    case 128: return plane_g_run_128(kp, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+    case 256: return plane_g_run_256(kp, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+    case 512: return plane_g_run_512(kp, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+    case 1024: return plane_g_run_1024(kp, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+// tuned kernels of the four hand-tuned geometries (storage order q' unless natural)
+static cudaError_t tuned_fwd(const tfno_cfg* c, const float2* x, float2* A, int64_t P, const float2* tw, bool nat,
+                             cudaStream_t st) {
+  const int dx = c->dim_x, kx = c->keep_x;
+  if (dx == 512) return fwd_rpt2() ? launch_fwd<G512f, 3>(x, A, P, tw, nat, st) : launch_fwd<G512, 3>(x, A, P, tw, nat, st);
+  if (dx == 256 && kx == 32) return launch_fwd<G256a, 4>(x, A, P, tw, nat, st);
+  if (dx == 256 && kx == 16) return launch_fwd<G256b, 4>(x, A, P, tw, nat, st);
+  if (dx == 128) return launch_fwd<G128, 4>(x, A, P, tw, nat, st);
+  return cudaErrorNotSupported;
+}
+static cudaError_t tuned_inv(const tfno_cfg* c, const float2* Cm, float2* y, int64_t P, const float2* tw, float scale,
+                             bool nat, cudaStream_t st) {
+  const int dx = c->dim_x, kx = c->keep_x;
+  if (dx == 512) return inv512_half() ? launch_inv<G512i, 3>(Cm, y, P, tw, scale, nat, st)
+                                      : launch_inv<G512, 3>(Cm, y, P, tw, scale, nat, st);
+  if (dx == 256 && kx == 32) return inv256a_8() ? launch_inv<G256a8, 2>(Cm, y, P, tw, scale, nat, st)
+                                                : launch_inv<G256a, 2>(Cm, y, P, tw, scale, nat, st);
+  if (dx == 256 && kx == 16) return inv256b_8() ? launch_inv<G256b8, 2>(Cm, y, P, tw, scale, nat, st)
+                                                : launch_inv<G256b, 2>(Cm, y, P, tw, scale, nat, st);
+  if (dx == 128) return launch_inv<G128, 2>(Cm, y, P, tw, scale, nat, st);
+  return cudaErrorNotSupported;
+}
+
+// which kernels run the generic code (bit 0 forward, bit 1 inverse): always
+// both outside the tuned geometries; there the measured winner per kernel
+// (profiles/r02/plane_mix.txt), TFNO_PLANE_GENERIC=0..3 overrides for A/B
+static int plane_mix(const tfno_cfg* c) {
+  if (!plane2d_tuned(c)) return 3;
+  const int env = plane_generic_env();
+  if (env >= 0) return env & 3;
+  return c->dim_x == 512 ? 1 : 0;
+}
+
 cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw,
                                cudaStream_t st) {
-  const int dx = c->dim_x, kx = c->keep_x;
   const int64_t P = (int64_t)c->batch * c->hidden_dim;
-  if (dx == 512) return fwd_rpt2() ? launch_fwd<G512f, 3>(x, modes, P, tw, true, st) : launch_fwd<G512, 3>(x, modes, P, tw, true, st);
-  if (dx == 256 && kx == 32) return launch_fwd<G256a, 4>(x, modes, P, tw, true, st);
-  if (dx == 256 && kx == 16) return launch_fwd<G256b, 4>(x, modes, P, tw, true, st);
-  if (dx == 128) return launch_fwd<G128, 4>(x, modes, P, tw, true, st);
-  return cudaErrorNotSupported;
+  if (plane_mix(c) & 1) return plane_g_run(c, -1, x, modes, P, tw, 1.0f, st);
+  return tuned_fwd(c, x, modes, P, tw, true, st);
 }
 
 cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y, float scale, const float2* tw,
                                cudaStream_t st) {
-  const int dx = c->dim_x, kx = c->keep_x;
   const int64_t P = (int64_t)c->batch * c->output_dim;
-  if (dx == 512) return launch_inv<G512, 3>(modes, y, P, tw, scale, true, st);
-  if (dx == 256 && kx == 32) return launch_inv<G256a, 2>(modes, y, P, tw, scale, true, st);
-  if (dx == 256 && kx == 16) return launch_inv<G256b, 2>(modes, y, P, tw, scale, true, st);
-  if (dx == 128) return launch_inv<G128, 2>(modes, y, P, tw, scale, true, st);
-  return cudaErrorNotSupported;
+  if (plane_mix(c) & 2) return plane_g_run(c, 1, modes, y, P, tw, scale, st);
+  return tuned_inv(c, modes, y, P, tw, scale, true, st);
 }
 
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
                                  float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t st,
                                  void (*mark)(cudaStream_t)) {
-  const int dx = c->dim_x, kx = c->keep_x;
-  if (dx == 512) {
-    if (inv512_half()) return run_pair<G512, 3, 3, G512f, G512i>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-    return fwd_rpt2() ? run_pair<G512, 3, 3, G512f>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
-                      : run_pair<G512, 3, 3>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  }
-  if (dx == 256 && kx == 32)
-    return inv256a_8() ? run_pair<G256a, 4, 2, G256a, G256a8>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
-                       : run_pair<G256a, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  if (dx == 256 && kx == 16)
-    return inv256b_8() ? run_pair<G256b, 4, 2, G256b, G256b8>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark)
-                       : run_pair<G256b, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  if (dx == 128) return run_pair<G128, 4, 2>(c, x, w, y, A, Cm, tw, prec, wimg, st, mark);
-  return cudaErrorNotSupported;
+  const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
+  const int mix = plane_mix(c);
+  const bool nat = mix != 0;  // the generic kernels use the natural mode order; the tuned pair its own
+  cudaError_t e = (mix & 1) ? plane_g_run(c, -1, x, A, B * H, tw, 1.0f, st) : tuned_fwd(c, x, A, B * H, tw, nat, st);
+  if (e != cudaSuccess) return e;
+  if (mark) mark(st);
+  // channel mixing over modes, 1/(dx*dy) folded into alpha (the mix is order-agnostic)
+  const int64_t MQ = plane2d_modes(c);
+  GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ,
+              (float)(1.0 / ((double)c->dim_x * c->dim_y))};
+  ga.wimg = wimg;
+  if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e;
+  if (mark) mark(st);
+  e = (mix & 2) ? plane_g_run(c, 1, Cm, y, B * N, tw, 1.0f, st) : tuned_inv(c, Cm, y, B * N, tw, 1.0f, nat, st);
+  if (e != cudaSuccess) return e;
+  if (mark) mark(st);
+  return cudaSuccess;
 }
 
 }  // namespace tfno

@@ -6,6 +6,11 @@
 
 namespace tfno {
 bool plane2d_supported(const tfno_cfg* c);
+// mode count per plane of the A / C workspace tensors (kx*ky, or KP^2 on the generic kernels)
+int64_t plane2d_modes(const tfno_cfg* c);
+// the natural [kx][ky] mode layout of the spectrum API is what the plane kernels produce
+bool plane2d_spectrum_ok(const tfno_cfg* c);
+int plane_g_kp(const tfno_cfg* c);
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
                                  float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t s,
                                  void (*mark)(cudaStream_t));

@@ -1,0 +1,122 @@
+// Launchers for the generic per-plane 2D kernels (plane_g.cuh): one
+// instantiation per (dy, KP) with dy in {64 ... 1024}, KP in {8 ... 128}.
+// Each translation unit compiles the dy values listed in PLANE_G_DYS so the
+// build parallelises; plane_g_dispatch.cu routes a config to the right unit.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "plane2d.cuh"
+#include "plane_g.cuh"
+
+#ifndef PLANE_G_DY
+#error "compile with -DPLANE_G_DY=<dy>"
+#endif
+
+namespace tfno {
+
+namespace {
+
+template <int DY, int KP>
+struct PGCfg {
+  static constexpr int V = DY >= 256 ? 16 : 8;
+  static constexpr int M = DY / V;
+  static constexpr int CAPF = KP >= 128 ? 128 : 256;
+  static constexpr int NTHF = M * (KP < CAPF / M ? KP : CAPF / M);
+  static constexpr int NTHI = M * (KP < 256 / M ? KP : 256 / M);
+  static constexpr int S = KP >= 128 ? 2 : 3;
+  static constexpr bool BIG = KP >= 128;  // accumulate classes in global, mode tile read from L2
+  using GF = PG<DY, KP, KP, NTHF>;
+  using GI = PG<DY, KP, KP, NTHI>;
+};
+
+template <class G>
+size_t g_fwd_smem(int S, int dx) {
+  return sizeof(float2) * ((size_t)S * G::TEAMS * G::DY + 2 * (size_t)G::TB + (size_t)G::KXP * G::KYP + G::DY +
+                           G::KXP + dx) +
+         16 * S + 16;
+}
+template <class G>
+size_t g_inv_smem(bool cing, int dx) {
+  return sizeof(float2) * ((cing ? 0 : (size_t)G::KXP * G::KYP) + (size_t)G::KXP * G::KYP + 2 * (size_t)G::TB +
+                           G::DY + G::KXP + dx) +
+         16;
+}
+
+template <class K>
+cudaError_t persistent_grid(K kernel, int threads, size_t smem, int64_t planes, int* grid) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem)) != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int64_t cap = (int64_t)device_sms() * occ;
+  *grid = (int)(planes < cap ? planes : cap);
+  return cudaSuccess;
+}
+
+template <int DY, int KP>
+cudaError_t g_fwd(const float2* x, float2* A, int64_t planes, int dx, int kx, int ky, const float2* tw,
+                  cudaStream_t st) {
+  using C = PGCfg<DY, KP>;
+  using G = typename C::GF;
+  if (planes <= 0) return cudaSuccess;
+  auto kern = plane_fwd_g<G, C::S, C::BIG>;
+  const size_t smem = g_fwd_smem<G>(C::S, dx);
+  int grid = 0;
+  cudaError_t e = persistent_grid(kern, G::NTH + 32, smem, planes, &grid);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, G::NTH + 32, smem, st>>>(x, A, planes, dx, kx, ky, tw);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <int DY, int KP>
+cudaError_t g_inv(const float2* Cm, float2* y, int64_t planes, int dx, const float2* tw, float scale,
+                  cudaStream_t st) {
+  using C = PGCfg<DY, KP>;
+  using G = typename C::GI;
+  if (planes <= 0) return cudaSuccess;
+  auto kern = plane_inv_g<G, C::BIG>;
+  const size_t smem = g_inv_smem<G>(C::BIG, dx);
+  int grid = 0;
+  cudaError_t e = persistent_grid(kern, G::NTH, smem, planes, &grid);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, G::NTH, smem, st>>>(Cm, y, planes, dx, tw, scale);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <int DY>
+cudaError_t g_dispatch(int KP, int dir, const float2* in, float2* out, int64_t planes, int dx, int kx, int ky,
+                       const float2* tw, float scale, cudaStream_t st) {
+#define TFNO_G_CASE(K)                                                                       \
+  case K:                                                                                    \
+    if constexpr (K <= DY)                                                                   \
+      return dir < 0 ? g_fwd<DY, K>(in, out, planes, dx, kx, ky, tw, st)                     \
+                     : g_inv<DY, K>(in, out, planes, dx, tw, scale, st);                     \
+    break;
+  switch (KP) {
+    TFNO_G_CASE(8)
+    TFNO_G_CASE(16)
+    TFNO_G_CASE(32)
+    TFNO_G_CASE(64)
+    TFNO_G_CASE(128)
+    default: break;
+  }
+#undef TFNO_G_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+#define TFNO_CAT2(a, b) a##b
+#define TFNO_CAT(a, b) TFNO_CAT2(a, b)
+// entry point of this translation unit: plane_g_run_<dy>
+cudaError_t TFNO_CAT(plane_g_run_, PLANE_G_DY)(int KP, int dir, const float2* in, float2* out, int64_t planes,
+                                               int dx, int kx, int ky, const float2* tw, float scale,
+                                               cudaStream_t st) {
+  return g_dispatch<PLANE_G_DY>(KP, dir, in, out, planes, dx, kx, ky, tw, scale, st);
+}
+
+}  // namespace tfno

@@ -1,0 +1,412 @@
+// Generic per-plane 2D Fourier-layer kernels (rank-2 fully_fused path) for any
+// power-of-two plane dy in {64 ... 1024}, dx in [KP, 1024], and any keep up to
+// 128 per axis (padded to KP = a power of two >= max(kx, ky, 8); the bins
+// p >= kx or q >= ky are written as exact zeros, so the channel mix and the
+// padded inverse see precisely the reference's first-keep spectrum).
+//
+// Same plane-per-CTA structure as plane2d.cu, with a row FFT that moves less
+// through shared memory.  A row of DY = V*M points (V = 16 for DY >= 256,
+// else 8) is held by a team of M threads, V points each:
+//   stage 1  V-point DFT in registers over y2 (x[tt + M*y2]), twiddle
+//            w_DY^{r*tt}, ONE transpose through shared memory;
+//   stage 2  thread (r, a) (A = M/V lanes per sequence) takes the V values
+//            tt = a + A*c, V-point DFT over c, twiddle w_M^{k*a}; the sum over
+//            a is a reduce-scatter across the A lanes with warp shuffles
+//            (A <= 4), so only the kept bins q = r + V*k < KY leave registers.
+// The reference does the same math as x-FFT | y-FFT (pipeline.py:149-206);
+// SURVEY.md Appendix A.  x direction: four-step classes x = x0 + R*x1
+// (R = dx/KP) exactly as in plane2d.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace tfno {
+
+template <int DY_, int KXP_, int KYP_, int NTH_>
+struct PG {
+  static constexpr int DY = DY_, KXP = KXP_, KYP = KYP_, NTH = NTH_;
+  static constexpr int V = DY >= 256 ? 16 : 8;  // points per thread in the row FFT
+  static constexpr int M = DY / V;              // threads per row team
+  static constexpr int A = M / V;               // lanes per sequence in stage 2
+  static constexpr int T = KYP >= V ? KYP / V : 1;  // kept bins per sequence
+  static constexpr int RN = KYP >= V ? V : KYP;     // sequences with kept bins
+  static constexpr int TEAMS = NTH / M;
+  static constexpr int KA = KXP / 8;  // column FFT: radix 8 x radix KA
+  static constexpr int IPC = KXP / TEAMS;  // row iterations per class
+  static constexpr int TS = M + A;         // transpose stride: == A (mod 16) -> conflict-free
+  static constexpr int TB = TEAMS * V * TS;
+  static constexpr int TASKS2 = (8 * KYP + NTH - 1) / NTH;
+  static constexpr int F = T >= A ? T / A : 1;  // kept bins per lane after the reduce
+  static_assert(A >= 1 && M == A * V, "row geometry");
+  static_assert(NTH % M == 0 && TEAMS >= 1 && KXP % TEAMS == 0, "teams");
+  static_assert(KXP >= 8 && KA <= 16 && KYP <= DY && KYP >= 1, "keep");
+  static_assert(M <= 32 || M % 32 == 0, "team shape");
+};
+
+template <int M>
+__device__ __forceinline__ void gteam_sync(int team) {
+  if constexpr (M <= 32)
+    __syncwarp();
+  else
+    named_bar(1 + team, M);
+}
+constexpr int kGComputeBar = 15;
+
+// reduce-scatter of CNT values over the lane bits S, S/2, ..., 1: the lane
+// with bit S set keeps the upper half; `off` = first kept index
+template <int CNT, int S>
+__device__ __forceinline__ void lane_reduce(float2* v, int a, int& off) {
+  if constexpr (S >= 1) {
+    const bool hi = (a & S) != 0;
+    if constexpr (CNT >= 2) {
+      constexpr int H = CNT / 2;
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        const float2 send = hi ? v[i] : v[i + H];
+        const float2 keep = hi ? v[i + H] : v[i];
+        v[i] = cadd(keep, shfl_xor2(send, S));
+      }
+      if (hi) off += H;
+      lane_reduce<H, S / 2>(v, a, off);
+    } else {
+      v[0] = cadd(v[0], shfl_xor2(v[0], S));
+      lane_reduce<1, S / 2>(v, a, off);
+    }
+  }
+}
+
+// ============================================================== forward
+// x[plane] (dx*DY) -> A[plane][KXP][KYP] (natural order, masked to kx x ky)
+template <class G, int S, bool ACCG>
+__global__ void __launch_bounds__(G::NTH + 32, 1)
+    plane_fwd_g(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes, int dx, int kx, int ky,
+                const float2* __restrict__ twg) {
+  constexpr int DY = G::DY, V = G::V, M = G::M, A = G::A, T = G::T, RN = G::RN, TEAMS = G::TEAMS;
+  constexpr int KXP = G::KXP, KYP = G::KYP, KA = G::KA, IPC = G::IPC, TS = G::TS, NTH = G::NTH, F = G::F;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* ring = reinterpret_cast<float2*>(smem);  // S x TEAMS x DY
+  float2* tb = ring + S * TEAMS * DY;              // 2 x TB (double-buffered transpose)
+  float2* Tc = tb + 2 * G::TB;                     // KXP x KYP class buffer
+  float2* twy = Tc + KXP * KYP;                    // w_DY^k
+  float2* twk = twy + DY;                          // w_KXP^k
+  float2* twx = twk + KXP;                         // w_dx^k
+  uint64_t* full = reinterpret_cast<uint64_t*>(twx + dx);
+  uint64_t* empty = full + S;
+
+  const int tid = threadIdx.x;
+  const int R = dx / KXP;
+  const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  for (int k = tid; k < DY; k += blockDim.x) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]);
+  for (int k = tid; k < KXP; k += blockDim.x) twk[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / KXP)]);
+  for (int k = tid; k < dx; k += blockDim.x) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / dx)]);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NTH / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= NTH) {
+    // ---------------- producer warp: TEAMS rows per ring slot, class by class
+    if (tid == NTH) {
+      const uint64_t pol = policy_evict_first();
+      int slot = 0, cnt = 0;
+      uint32_t phase = 0;
+      for (int64_t kp = 0; kp < nmine; ++kp) {
+        const float2* src = x + (blockIdx.x + kp * gridDim.x) * (int64_t)dx * DY;
+        for (int x0 = 0; x0 < R; ++x0) {
+          for (int j = 0; j < IPC; ++j, ++cnt) {
+            if (cnt >= S) mbar_wait(&empty[slot], phase ^ 1u);
+            float2* dst = ring + slot * TEAMS * DY;
+            mbar_expect_tx(&full[slot], TEAMS * DY * 8);
+#pragma unroll 1
+            for (int tm = 0; tm < TEAMS; ++tm)
+              tma_load_1d(dst + tm * DY, src + (int64_t)(x0 + R * (j * TEAMS + tm)) * DY, DY * 8, &full[slot], pol);
+            if (++slot == S) {
+              slot = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute threads
+  const int team = tid / M, tt = tid % M;
+  const int r_ = tt / A, a_ = tt % A;
+  float2 tw1[V];
+#pragma unroll
+  for (int r = 0; r < V; ++r) tw1[r] = twy[r * tt];
+  float2 tw3[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) tw3[k] = twy[(V * k * a_) % DY];
+  // stage-2 output validity: lanes holding a kept bin after the reduce
+  const bool st_ok = (r_ < RN) && (T >= A || (a_ % (A / (T < A ? T : A))) == 0);
+
+  float2 acc[ACCG ? 1 : G::TASKS2][ACCG ? 1 : KA];
+  if constexpr (!ACCG) {
+#pragma unroll
+    for (int a = 0; a < G::TASKS2; ++a)
+#pragma unroll
+      for (int u = 0; u < KA; ++u) acc[a][u] = make_float2(0.f, 0.f);
+  }
+
+  int slot = 0, buf = 0;
+  uint32_t phase = 0;
+  for (int64_t kp = 0; kp < nmine; ++kp) {
+    const int64_t pl = blockIdx.x + kp * gridDim.x;
+    float2* dstA = Aout + pl * (int64_t)KXP * KYP;
+#pragma unroll 1
+    for (int x0 = 0; x0 < R; ++x0) {
+#pragma unroll 1
+      for (int j = 0; j < IPC; ++j) {
+        mbar_wait(&full[slot], phase);
+        float2* tbt = tb + buf * G::TB + team * V * TS;
+        // ---- stage 1: V-point DFT over y2, twiddle w_DY^{r tt}, transpose
+        {
+          float2 v[V];
+          const float2* row = ring + slot * TEAMS * DY + team * DY;
+#pragma unroll
+          for (int y2 = 0; y2 < V; ++y2) v[y2] = row[tt + M * y2];
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+          dft<V, -1>(v);
+#pragma unroll
+          for (int r = 1; r < V; ++r) v[r] = cmul(v[r], tw1[r]);
+#pragma unroll
+          for (int r = 0; r < RN; ++r) tbt[r * TS + tt] = v[r];
+        }
+        gteam_sync<M>(team);
+        // ---- stage 2: V-point DFT over c, twiddle w_M^{k a}, reduce over the A lanes
+        {
+          float2 u[V];
+#pragma unroll
+          for (int c = 0; c < V; ++c) u[c] = tbt[(r_ < RN ? r_ : 0) * TS + a_ + A * c];
+          float2 vals[T];
+          if constexpr (T == 1) {
+            float2 s0 = u[0], s1 = u[1];
+#pragma unroll
+            for (int c = 2; c < V; c += 2) {
+              s0 = cadd(s0, u[c]);
+              s1 = cadd(s1, u[c + 1]);
+            }
+            vals[0] = cadd(s0, s1);
+          } else {
+            dft<V, -1>(u);
+#pragma unroll
+            for (int k = 0; k < T; ++k) vals[k] = (A > 1 && k > 0) ? cmul(u[k % V], tw3[k]) : u[k % V];
+          }
+          int off = 0;
+          lane_reduce<T, A / 2>(vals, a_, off);
+          if (st_ok) {
+            const int x1 = j * TEAMS + team;
+#pragma unroll
+            for (int i = 0; i < F; ++i) Tc[x1 * KYP + r_ + V * (off + i)] = vals[i];
+          }
+        }
+        buf ^= 1;
+        if (++slot == S) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }  // j: rows of class x0
+      named_bar(kGComputeBar, NTH);
+      // ---- class x0 complete: KXP-point column FFT, pass 1 (radix 8 over m)
+      for (int tau = tid; tau < KA * KYP; tau += NTH) {
+        const int q = tau % KYP, i = tau / KYP;
+        float2 v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = Tc[(i + KA * m) * KYP + q];
+        dft8<-1>(v);
+        if (KA > 1) {
+#pragma unroll
+          for (int s2 = 1; s2 < 8; ++s2) v[s2] = cmul(v[s2], twk[i * s2]);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) Tc[(s2 * KA + i) * KYP + q] = v[s2];
+      }
+      named_bar(kGComputeBar, NTH);
+      // pass 2 (radix KA over i) + four-step twiddle w_dx^{p x0}, accumulate
+#pragma unroll
+      for (int jj = 0; jj < G::TASKS2; ++jj) {
+        const int tau = tid + jj * NTH;
+        if (tau < 8 * KYP) {
+          const int q = tau % KYP, s2 = tau / KYP;
+          float2 w[KA];
+#pragma unroll
+          for (int i = 0; i < KA; ++i) w[i] = Tc[(s2 * KA + i) * KYP + q];
+          dft<KA, -1>(w);
+          if constexpr (ACCG) {
+            // large keeps: accumulate the classes in the (L2-resident) output tile
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+              const int p = s2 + 8 * u;
+              float2* d = dstA + p * KYP + q;
+              if (p >= kx || q >= ky) {
+                if (x0 == 0) *d = make_float2(0.f, 0.f);
+              } else if (x0 == 0) {
+                *d = w[u];
+              } else {
+                float2 o = *d;
+                cmac(o, w[u], twx[p * x0]);
+                *d = o;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < KA; ++u) cmac(acc[jj][u], w[u], twx[(s2 + 8 * u) * x0]);
+          }
+        }
+      }
+      named_bar(kGComputeBar, NTH);
+      if constexpr (!ACCG) {
+        if (x0 == R - 1) {
+#pragma unroll
+          for (int jj = 0; jj < G::TASKS2; ++jj) {
+            const int tau = tid + jj * NTH;
+            if (tau < 8 * KYP) {
+              const int q = tau % KYP, s2 = tau / KYP;
+#pragma unroll
+              for (int u = 0; u < KA; ++u) {
+                const int p = s2 + 8 * u;
+                dstA[p * KYP + q] = (p < kx && q < ky) ? acc[jj][u] : make_float2(0.f, 0.f);
+                acc[jj][u] = make_float2(0.f, 0.f);
+              }
+            }
+          }
+        }
+      }
+    }  // x0
+  }  // planes
+}
+
+// ============================================================== inverse
+// C[plane][KXP][KYP] -> y[plane] (dx*DY), scaled by `scale`.  CING: the mode
+// tile is read from global (L2) per class instead of being staged in smem.
+template <class G, bool CING>
+__global__ void __launch_bounds__(G::NTH, 1)
+    plane_inv_g(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes, int dx,
+                const float2* __restrict__ twg, float scale) {
+  constexpr int DY = G::DY, V = G::V, M = G::M, A = G::A, T = G::T, RN = G::RN, TEAMS = G::TEAMS;
+  constexpr int KXP = G::KXP, KYP = G::KYP, KA = G::KA, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* cin = reinterpret_cast<float2*>(smem);  // KXP x KYP (TMA target; unused if CING)
+  float2* Gb = cin + (CING ? 0 : KXP * KYP);      // KXP x KYP
+  float2* tb = Gb + KXP * KYP;                    // 2 x TB
+  float2* twy = tb + 2 * G::TB;                   // conj w_DY^k
+  float2* twk = twy + DY;                         // conj w_KXP^k
+  float2* twx = twk + KXP;                        // scale * conj w_dx^k
+  uint64_t* bar = reinterpret_cast<uint64_t*>(twx + dx);
+
+  const int tid = threadIdx.x;
+  const int R = dx / KXP;
+  const int team = tid / M, tt = tid % M;
+  const int r_ = tt / A, a_ = tt % A;
+  const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  for (int k = tid; k < DY; k += NTH) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]));
+  for (int k = tid; k < KXP; k += NTH) twk[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / KXP)]));
+  for (int k = tid; k < dx; k += NTH) twx[k] = cscale(conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / dx)])), scale);
+  if (!CING && tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int64_t k) {
+    const int64_t pl = blockIdx.x + k * gridDim.x;
+    mbar_expect_tx(bar, KXP * KYP * 8);
+    tma_load_1d(cin, Cin + pl * (int64_t)KXP * KYP, KXP * KYP * 8, bar, pol);
+  };
+  if (!CING && tid == 0 && nmine > 0) issue(0);
+
+  float2 tw1[V], tw3[T];
+#pragma unroll
+  for (int r = 0; r < V; ++r) tw1[r] = twy[r * tt];
+#pragma unroll
+  for (int k = 0; k < T; ++k) tw3[k] = twy[(V * k * a_) % DY];
+  int buf = 0;
+  for (int64_t k = 0; k < nmine; ++k) {
+    const int64_t pl = blockIdx.x + k * gridDim.x;
+    const float2* src = CING ? Cin + pl * (int64_t)KXP * KYP : cin;
+    if (!CING) mbar_wait(bar, (uint32_t)(k & 1));
+    float2* yp = y + pl * (int64_t)dx * DY;
+    for (int x0 = 0; x0 < R; ++x0) {
+      named_bar(kGComputeBar, NTH);  // previous class's rows are done with Gb
+      // ---- column iFFT, pass 1: twiddle w_dx^{+p x0} (carries the scale), radix KA over u
+      for (int tau = tid; tau < 8 * KYP; tau += NTH) {
+        const int q = tau % KYP, s2 = tau / KYP;
+        float2 w[KA];
+#pragma unroll
+        for (int u = 0; u < KA; ++u) {
+          const int p = s2 + 8 * u;
+          const float2 cv = CING ? __ldg(&src[p * KYP + q]) : src[p * KYP + q];
+          w[u] = cmul(cv, twx[p * x0]);
+        }
+        dft<KA, 1>(w);
+#pragma unroll
+        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twk[s2 * i]);
+#pragma unroll
+        for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KYP + q] = w[i];
+      }
+      named_bar(kGComputeBar, NTH);
+      if (!CING && x0 == R - 1 && tid == 0 && k + 1 < nmine) issue(k + 1);  // cin fully consumed
+      // pass 2: radix 8 over s2 -> rows x1 = i + KA*m
+      for (int tau = tid; tau < KA * KYP; tau += NTH) {
+        const int q = tau % KYP, i = tau / KYP;
+        float2 v[8];
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) v[s2] = Gb[(s2 * KA + i) * KYP + q];
+        dft8<1>(v);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KYP + q] = v[m];
+      }
+      named_bar(kGComputeBar, NTH);
+#pragma unroll 1
+      for (int j = 0; j < IPC; ++j) {
+        const int x1 = j * TEAMS + team;
+        float2* tbt = tb + buf * G::TB + team * V * TS;
+        // ---- stage A: (r, a) -- bins r + V*k (k < T), twiddle w_M^{+k a}, V-point iDFT over k
+        if (r_ < RN) {
+          float2 u[V];
+#pragma unroll
+          for (int c = 0; c < V; ++c) u[c] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < T; ++k) {
+            float2 g = Gb[x1 * KYP + r_ + V * k];
+            if (A > 1 && k > 0) g = cmul(g, tw3[k]);
+            u[k % V] = (k < V) ? g : cadd(u[k % V], g);
+          }
+          dft_in<V, 1, (T < V ? T : V)>(u);
+#pragma unroll
+          for (int c = 0; c < V; ++c) tbt[r_ * TS + a_ + A * c] = u[c];
+        }
+        gteam_sync<M>(team);
+        // ---- stage B: thread tt -- twiddle w_DY^{+r tt}, V-point iDFT over r, streaming stores
+        {
+          float2 v[V];
+#pragma unroll
+          for (int r = 0; r < V; ++r) v[r] = r < RN ? tbt[r * TS + tt] : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int r = 1; r < RN; ++r) v[r] = cmul(v[r], tw1[r]);
+          dft_in<V, 1, RN>(v);
+          float2* orow = yp + (int64_t)(x0 + R * x1) * DY;
+#pragma unroll
+          for (int y2 = 0; y2 < V; ++y2) __stcs(orow + tt + M * y2, v[y2]);
+        }
+        buf ^= 1;
+      }
+    }
+  }
+}
+
+}  // namespace tfno

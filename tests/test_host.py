@@ -118,8 +118,13 @@ def test_schedules_and_workspace():
     c2b = T.FnoLayerConfig(1024, 256, 256, 1, 4096, 1, 512, 1)
     assert T.layer_schedule(c2b, "fully_fused") == (3, "y-fft|cgemm|y-ifft")
     assert T.layer_schedule(c1, "fft_optimized")[0] == 3
-    r2 = T.FnoLayerConfig(2, 16, 16, 32, 64, 8, 16, 2)
-    assert T.layer_schedule(r2, "fully_fused") == (3, "x-fft|fused-fft-cgemm-ifft|x-ifft")
+    r2 = T.FnoLayerConfig(2, 16, 16, 32, 64, 8, 16, 2)  # generic plane kernels (dy >= 64, KP = 16 <= dx)
+    assert T.layer_schedule(r2, "fully_fused") == (3, "plane-fft2d|cgemm-modes|plane-ifft2d")
+    # ragged keeps pad to KP = 32 modes per axis in the A / C workspace tensors
+    r3 = T.FnoLayerConfig(2, 16, 8, 256, 128, 20, 12, 2)
+    assert T.workspace_bytes(r3, "fully_fused") == 2 * (16 + 8) * 32 * 32 * 8
+    r4 = T.FnoLayerConfig(2, 16, 16, 64, 32, 8, 16, 2)  # dy < 64: the paper schedule
+    assert T.layer_schedule(r4, "fully_fused") == (3, "x-fft|fused-fft-cgemm-ifft|x-ifft")
     f = T.layer_flops(c4)
     assert f["bytes"] == 8 * (2 * 128 * 128 * 512 * 512 + 128 * 128)
 

@@ -83,7 +83,8 @@ def summarize(csv_path, order_path=None):
             val = float(v)
         except ValueError:
             continue
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6,
+                 "ms": 1e-3,
                  "msecond": 1e-3, "second": 1.0}.get(r["Metric Unit"], 1.0)
         k["m"][r["Metric Name"]] = val * scale
     # every bracket starts with the marker kernel: split the launch sequence there

@@ -105,6 +105,20 @@ size_t tfno_workspace_bytes(const tfno_cfg* cfg, int mode, int prec);
 int tfno_layer_forward(const tfno_cfg* cfg, int mode, int prec, const void* x, const void* w, void* y,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Tensor-core weight packing (SURVEY.md §8b tfno_prepare_weights; no reference
+ * equivalent -- the reference's W is a plain ComplexMatrix, cgemm.py:21-58).
+ * The real-embedded W' image [[Wr, Wi], [-Wi, Wr]] of W[H][N] in the exact
+ * shared-memory layout of the tcgen05 contraction (TF32 / 3xTF32: hi and lo
+ * tiles; BF16), built once per weight tensor instead of once per call.
+ * tfno_packed_weight_bytes: 0 for TFNO_FP32 (the SIMT path needs no packing).
+ * w_packed must be 16-byte aligned device memory. */
+size_t tfno_packed_weight_bytes(const tfno_cfg* cfg, int prec);
+int tfno_prepare_weights(const tfno_cfg* cfg, int prec, const void* w, void* w_packed, void* stream);
+/* tfno_layer_forward with W' from tfno_prepare_weights (same cfg.hidden_dim /
+ * output_dim and prec): skips the per-call image build launch. */
+int tfno_layer_forward_packed(const tfno_cfg* cfg, int mode, int prec, const void* x, const void* w,
+                              const void* w_packed, void* y, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Spectrum-level entry points (building blocks of the hidden-dim split and
  * of layer chains).  modes are natural-order [planes][keep_x][keep_y] c64.
  *   forward: modes[B][H] = first-keep 2D (rank 2) / 1D (rank 1) DFT of x[B][H]

@@ -18,7 +18,8 @@ from .fft import (FORWARD, INVERSE, FftPlan, InvalidKeep, InvalidLength, Invalid
 from .cgemm import ComplexMatrix, GemmProblem, cgemm_device, gemm_kloop, gemm_tiled  # noqa: F401
 from .pipeline import (ARRAY_NAMES, MODES, ConfigMismatch, FusedSchedule, ScheduleInvalid,  # noqa: F401
                        TrafficDelta, TrafficLedger, build_schedule, layer_flops, layer_op_stats,
-                       layer_schedule, model_ledger, run_fused, run_layer, run_layer_device, run_staged,
+                       PackedWeights, layer_schedule, model_ledger, prepare_weights, run_fused, run_layer,
+                       run_layer_device, run_staged,
                        traffic_delta, workspace_bytes)
 
 from .autograd import layer_backward, spectral_layer  # noqa: F401,E402  (backward pass, §8f row 4)

@@ -44,6 +44,10 @@ _SIGS = {
     "tfno_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int]),
     "tfno_layer_forward": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int, _VP, _VP, _VP,
                                           _VP, ctypes.c_size_t, _VP]),
+    "tfno_packed_weight_bytes": (ctypes.c_size_t, [ctypes.POINTER(TfnoCfg), ctypes.c_int]),
+    "tfno_prepare_weights": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, _VP, _VP, _VP]),
+    "tfno_layer_forward_packed": (ctypes.c_int, [ctypes.POINTER(TfnoCfg), ctypes.c_int, ctypes.c_int, _VP, _VP, _VP,
+                                                 _VP, _VP, ctypes.c_size_t, _VP]),
     "tfno_fft_execute": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _VP,
                                         _I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
     "tfno_cgemm": (ctypes.c_int, [_I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _VP, _I64, _I64, _I64,

@@ -621,8 +621,45 @@ int tfno_spectrum_inverse(const tfno_cfg* c, const void* modes, void* yv, float 
   return TFNO_OK;
 }
 
+size_t tfno_packed_weight_bytes(const tfno_cfg* c, int prec) {
+  if (!c || tfno_config_violations(c, nullptr, 8)) return 0;
+  if (prec != TFNO_TF32 && prec != TFNO_TF32X3 && prec != TFNO_BF16) return 0;
+  return cgemm_tc_wimg_bytes(c->output_dim, c->hidden_dim, prec);
+}
+
+int tfno_prepare_weights(const tfno_cfg* c, int prec, const void* wv, void* packed, void* stream) {
+  if (!c || tfno_config_violations(c, nullptr, 8) || !wv || !packed) return TFNO_EINVAL;
+  if (prec != TFNO_TF32 && prec != TFNO_TF32X3 && prec != TFNO_BF16) return TFNO_EINVAL;
+  if (((uintptr_t)packed & 15) != 0) return TFNO_EINVAL;
+  GemmArgs ga{};
+  ga.M = 1;
+  ga.N = c->output_dim;
+  ga.K = c->hidden_dim;
+  ga.batch = 1;
+  ga.a_ms = 1;
+  ga.W = (const float2*)wv;
+  ga.w_ks = c->output_dim;
+  ga.w_ns = 1;
+  ga.c_ms = 1;
+  return cuda_status(build_cgemm_wimg(ga, prec, packed, (cudaStream_t)stream));
+}
+
+static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv,
+                              const void* packed, void* yv, void* wsv, size_t ws_bytes, void* stream);
+
 int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv, void* yv,
                        void* wsv, size_t ws_bytes, void* stream) {
+  return layer_forward_impl(c, mode, prec, xv, wv, nullptr, yv, wsv, ws_bytes, stream);
+}
+
+int tfno_layer_forward_packed(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv,
+                              const void* w_packed, void* yv, void* wsv, size_t ws_bytes, void* stream) {
+  if (!w_packed || ((uintptr_t)w_packed & 15) != 0) return TFNO_EINVAL;
+  return layer_forward_impl(c, mode, prec, xv, wv, w_packed, yv, wsv, ws_bytes, stream);
+}
+
+static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void* xv, const void* wv,
+                              const void* packed, void* yv, void* wsv, size_t ws_bytes, void* stream) {
   if (!c || mode < TFNO_STAGED || mode > TFNO_FULLY_FUSED) return TFNO_EINVAL;
   if (tfno_config_violations(c, nullptr, 8)) return TFNO_EINVAL;
   if (prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3 && prec != TFNO_BF16) return TFNO_EINVAL;
@@ -672,10 +709,14 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
   const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;
   if (s.need_A) { A = p; p += g.B * g.H * mq; }
   if (s.need_C) { Cm = p; p += g.B * g.N * mq; }
-  void* wimg = (wimg_need && ws_bytes >= need + wimg_need) ? (void*)p : nullptr;
+  // W' image: the caller's packed weights (tfno_prepare_weights) or built per call in the workspace tail
+  const int wimg_ready = (packed && wimg_need) ? 1 : 0;
+  void* wimg = wimg_ready ? const_cast<void*>(packed)
+                          : ((wimg_need && ws_bytes >= need + wimg_need) ? (void*)p : nullptr);
 
   stage_begin(st);
-  if (s.plane2d) return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, st, &stage_mark));
+  if (s.plane2d)
+    return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, wimg_ready, st, &stage_mark));
 
   cudaError_t e;
   const float2* src = x;
@@ -744,6 +785,7 @@ int tfno_layer_forward(const tfno_cfg* c, int mode, int prec, const void* xv, co
     GemmArgs ga{g.kx * g.ky, g.N, g.H, g.B, A, 1, g.kx * g.ky, g.H * g.kx * g.ky, w, g.N, 1, 0,
                 Cm, 1, g.kx * g.ky, g.N * g.kx * g.ky, 1.0f};
     ga.wimg = wimg;
+    ga.wimg_ready = wimg_ready;
     if (g.B > 65535) return TFNO_EUNSUPPORTED;
     if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e == cudaErrorNotSupported ? TFNO_EUNSUPPORTED : TFNO_ECUDA;
     stage_mark(st);

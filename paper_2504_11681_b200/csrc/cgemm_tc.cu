@@ -666,6 +666,175 @@ __global__ void __launch_bounds__(128, 1) cgemm_tc_bf16_kernel(GemmArgs g) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
 }
 
+// BF16 W' image: per (output-channel block, K' chunk) the B tile exactly as it
+// sits in shared memory (K-major, core matrix 8 rows x 8 bf16): rows 2n =
+// (Wr, -Wi) and 2n+1 = (Wi, Wr) per channel.  Built once (per call, or once
+// per weight tensor by tfno_prepare_weights).
+template <int NP>
+__global__ void __launch_bounds__(256) wimg_bf16_kernel(GemmArgs g, uint8_t* img) {
+  constexpr int B_LBO = (NP / 8) * 128, BT = NP * TC_BK * 2;
+  const int64_t N = g.N, K = g.K;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));
+  const int64_t items = (int64_t)nsplit * nchunks * (NP / 2) * (TC_BK / 8);  // (n, channel quad)
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+    const int nl = (int)(it % (NP / 2));
+    const int hq = (int)((it / (NP / 2)) % (TC_BK / 8));
+    const int64_t blk = it / ((NP / 2) * (TC_BK / 8));
+    const int c = (int)(blk % nchunks);
+    const int64_t nb = blk / nchunks;
+    const int64_t h = (int64_t)c * (TC_BK / 2) + 4 * hq, n = nb * (NP / 2) + nl;
+    float2 w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = (n < N && h + q < K) ? g.W[(h + q) * g.w_ks + n] : make_float2(0.f, 0.f);
+    uint8_t* base = img + blk * BT;
+    *reinterpret_cast<uint4*>(base + cm_off16(2 * nl, 8 * hq, B_LBO)) =
+        make_uint4(tc::pack_bf16(w[0].x, -w[0].y), tc::pack_bf16(w[1].x, -w[1].y), tc::pack_bf16(w[2].x, -w[2].y),
+                   tc::pack_bf16(w[3].x, -w[3].y));
+    *reinterpret_cast<uint4*>(base + cm_off16(2 * nl + 1, 8 * hq, B_LBO)) =
+        make_uint4(tc::pack_bf16(w[0].y, w[0].x), tc::pack_bf16(w[1].y, w[1].x), tc::pack_bf16(w[2].y, w[2].x),
+                   tc::pack_bf16(w[3].y, w[3].x));
+  }
+}
+
+// BF16 contraction on the W' image: 256 threads stage A with 16-byte loads
+// (mode pair x channel quad per thread), one thread bulk-copies the chunk's
+// W' tile one chunk ahead; kind::f16 MMAs (K = 16) into the TMEM accumulator.
+template <int NP>
+__global__ void __launch_bounds__(256, 1) cgemm_tc_bf16_img_kernel(GemmArgs g) {
+  using Gm = TcGeo<NP>;
+  constexpr int AT = TC_BM * TC_BK * 2, BT = NP * TC_BK * 2;
+  constexpr int A_LBO = (TC_BM / 8) * 128, B_LBO = (NP / 8) * 128;
+  constexpr int STAGE = AT + BT;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);  // [2] MMA done, [2] W' landed
+  uint64_t* wbars = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = g.M, N = g.N, K = g.K;
+  const int mtiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int nsplit = (int)((N + NP / 2 - 1) / (NP / 2));
+  const int64_t tiles = (int64_t)mtiles * nsplit * g.batch;
+  const int nchunks = (int)((2 * K + TC_BK - 1) / TC_BK);
+  const uint8_t* img = reinterpret_cast<const uint8_t*>(g.wimg);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::saddr(tmem_slot)),
+                 "n"(Gm::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t IDESC = tc::make_idesc_bf16(TC_BM, NP);
+  // item = (mode pair mp < 64, channel quad hq < 4): 4 float4 loads -> rows m, m+1
+  float4 ra[4];
+  const bool vec = (M % 2 == 0) && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0);
+  const int mp = tid % (TC_BM / 2), hq = tid / (TC_BM / 2);
+  auto load_chunk = [&](int64_t t, int c) {
+    const int64_t b = t / ((int64_t)mtiles * nsplit);
+    const int64_t m = (t % mtiles) * TC_BM + 2 * mp;
+    const int64_t h = (int64_t)c * (TC_BK / 2) + 4 * hq;
+    const float2* Ab = g.A + b * g.a_bs;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t hh = h + q;
+      if (hh < K && m + 1 < M && vec) {
+        ra[q] = __ldg(reinterpret_cast<const float4*>(Ab + hh * g.a_ks + m));
+      } else {
+        const float2 u0 = (hh < K && m < M) ? __ldg(Ab + hh * g.a_ks + m) : make_float2(0.f, 0.f);
+        const float2 u1 = (hh < K && m + 1 < M) ? __ldg(Ab + hh * g.a_ks + m + 1) : make_float2(0.f, 0.f);
+        ra[q] = make_float4(u0.x, u0.y, u1.x, u1.y);
+      }
+    }
+  };
+  auto store_chunk = [&](int st) {
+    uint8_t* sA = stage_base + st * STAGE;
+    *reinterpret_cast<uint4*>(sA + cm_off16(2 * mp, 8 * hq, A_LBO)) =
+        make_uint4(tc::pack_bf16(ra[0].x, ra[0].y), tc::pack_bf16(ra[1].x, ra[1].y), tc::pack_bf16(ra[2].x, ra[2].y),
+                   tc::pack_bf16(ra[3].x, ra[3].y));
+    *reinterpret_cast<uint4*>(sA + cm_off16(2 * mp + 1, 8 * hq, A_LBO)) =
+        make_uint4(tc::pack_bf16(ra[0].z, ra[0].w), tc::pack_bf16(ra[1].z, ra[1].w), tc::pack_bf16(ra[2].z, ra[2].w),
+                   tc::pack_bf16(ra[3].z, ra[3].w));
+  };
+  auto w_issue = [&](int64_t t, int c, int st) {
+    const int64_t nbx = (t / mtiles) % nsplit;
+    bulk_g2s(stage_base + st * STAGE + AT, img + (nbx * nchunks + c) * (int64_t)BT, BT, &wbars[st]);
+  };
+  int64_t gch = 0;
+  int64_t tile = blockIdx.x;
+  if (tile < tiles) {
+    load_chunk(tile, 0);
+    if (tid == 0) w_issue(tile, 0, 0);
+  }
+  for (; tile < tiles; tile += gridDim.x) {
+    const int64_t nb = (tile / mtiles) % nsplit;
+    for (int c = 0; c < nchunks; ++c, ++gch) {
+      const int st = (int)(gch & 1);
+      if (gch >= 2) tc::mbar_wait(&bars[st], (uint32_t)(((gch - 2) >> 1) & 1));  // stage free
+      store_chunk(st);
+      if (c + 1 < nchunks)
+        load_chunk(tile, c + 1);
+      else if (tile + gridDim.x < tiles)
+        load_chunk(tile + gridDim.x, 0);
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc::mbar_wait(&wbars[st], (uint32_t)((gch >> 1) & 1));
+        tc::fence_after();
+        const uint32_t a0 = tc::saddr(stage_base + st * STAGE), b0 = a0 + AT;
+#pragma unroll
+        for (int s = 0; s < TC_BK / 16; ++s) {  // K = 16 per MMA = 2 K groups of 8
+          const uint64_t ad = tc::make_desc(a0 + 2 * s * A_LBO, A_LBO, 128);
+          const uint64_t bd = tc::make_desc(b0 + 2 * s * B_LBO, B_LBO, 128);
+          tc::mma_bf16(tmem, ad, bd, IDESC, (c > 0 || s > 0) ? 1u : 0u);
+        }
+        tc::commit(&bars[st]);
+        const bool more = c + 1 < nchunks || tile + gridDim.x < tiles;
+        if (more) {
+          if (gch >= 1) tc::mbar_wait(&bars[st ^ 1], (uint32_t)(((gch - 1) >> 1) & 1));
+          if (c + 1 < nchunks)
+            w_issue(tile, c + 1, st ^ 1);
+          else
+            w_issue(tile + gridDim.x, 0, st ^ 1);
+        }
+      }
+    }
+    {
+      const int64_t last = gch - 1;
+      tc::mbar_wait(&bars[last & 1], (uint32_t)((last >> 1) & 1));
+      tc::fence_after();
+      const int64_t b = tile / ((int64_t)mtiles * nsplit);
+      const int64_t n0 = nb * (NP / 2);
+      const int lw = warp & 3;
+      const int64_t m = (tile % mtiles) * TC_BM + lw * 32 + lane;
+      float2* Cb = g.C + b * g.c_bs;
+      const int cbeg = (warp >> 2) * (NP / 2), cend = cbeg + NP / 2;
+#pragma unroll 1
+      for (int col = cbeg; col < cend; col += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(lw * 32) << 16) + col, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t n = n0 + col / 2 + q;
+          if (m < M && n < N) Cb[n * g.c_ns + m] = make_float2(g.alpha * v[2 * q], g.alpha * v[2 * q + 1]);
+        }
+      }
+      tc::fence_before();
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Gm::TMEM_COLS) : "memory");
+}
+
 template <int NP>
 static cudaError_t launch_tc_bf16_t(const GemmArgs& g, cudaStream_t s) {
   const size_t smem = 2 * (TC_BM * TC_BK * 2 + NP * TC_BK * 2) + 64;
@@ -703,36 +872,69 @@ static size_t wimg_bytes_np(int64_t N, int64_t K, int passes) {
   return (size_t)(nsplit * nchunks * (passes > 1 ? 2 : 1) * TcGeo<NP>::B_TILE);
 }
 
+template <int NP>
+static size_t wimg_bf16_bytes_np(int64_t N, int64_t K) {
+  const int64_t nchunks = (2 * K + TC_BK - 1) / TC_BK, nsplit = (N + NP / 2 - 1) / (NP / 2);
+  return (size_t)(nsplit * nchunks * NP * TC_BK * 2);
+}
+
 size_t cgemm_tc_wimg_bytes(int64_t N, int64_t K, int prec) {
-  if (prec != 1 && prec != 3) return 0;  // TF32 / 3xTF32 only
-  const int passes = prec == 1 ? 1 : 3;
   const int np = (int)(2 * N);
+  if (prec == 2)  // BF16
+    return np <= 64 ? wimg_bf16_bytes_np<64>(N, K) : np <= 128 ? wimg_bf16_bytes_np<128>(N, K)
+                                                              : wimg_bf16_bytes_np<256>(N, K);
+  if (prec != 1 && prec != 3) return 0;  // TF32 / 3xTF32
+  const int passes = prec == 1 ? 1 : 3;
   return np <= 64 ? wimg_bytes_np<64>(N, K, passes) : np <= 128 ? wimg_bytes_np<128>(N, K, passes)
                                                                  : wimg_bytes_np<256>(N, K, passes);
 }
 
+// W' image builders (also the body of tfno_prepare_weights)
+template <int NP, int PASSES>
+static cudaError_t build_wimg_t(const GemmArgs& g, void* img, cudaStream_t s) {
+  const int sms = device_sms();
+  const int64_t nchunks = (2 * g.K + TC_BK - 1) / TC_BK, nsplit = (g.N + NP / 2 - 1) / (NP / 2);
+  const int64_t items = nsplit * nchunks * (NP / 2) * (TC_BK / (PASSES == 0 ? 8 : 4));
+  const int grid = (int)((items + 255) / 256 < 4 * sms ? (items + 255) / 256 : 4 * sms);
+  if (PASSES == 0)
+    wimg_bf16_kernel<NP><<<grid, 256, 0, s>>>(g, reinterpret_cast<uint8_t*>(img));
+  else
+    wimg_kernel<NP, (PASSES == 0 ? 1 : PASSES)><<<grid, 256, 0, s>>>(g, reinterpret_cast<uint8_t*>(img));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t build_cgemm_wimg(const GemmArgs& g, int prec, void* img, cudaStream_t s) {
+  if (!cgemm_tc_supported(g) || (prec != 1 && prec != 2 && prec != 3) || !img || ((uintptr_t)img & 15))
+    return cudaErrorNotSupported;
+  const int np = (int)(2 * g.N);
+  const int passes = prec == 2 ? 0 : prec == 1 ? 1 : 3;
+#define TFNO_WB(NPV)                                              \
+  if (passes == 0) return build_wimg_t<NPV, 0>(g, img, s);       \
+  if (passes == 1) return build_wimg_t<NPV, 1>(g, img, s);       \
+  return build_wimg_t<NPV, 3>(g, img, s);
+  if (np <= 64) { TFNO_WB(64) }
+  if (np <= 128) { TFNO_WB(128) }
+  TFNO_WB(256)
+#undef TFNO_WB
+}
+
+// contraction on a W' image in g.wimg: built here first unless g.wimg_ready
+// (tfno_prepare_weights built it once for this weight tensor).  PASSES 0 = BF16.
 template <int NP, int PASSES>
 static cudaError_t launch_tc_img_t(const GemmArgs& g, cudaStream_t s) {
-  constexpr int STAGE = (PASSES > 1 ? 2 : 1) * (TcGeo<NP>::A_TILE + TcGeo<NP>::B_TILE);
+  constexpr int STAGE = PASSES == 0 ? TC_BM * TC_BK * 2 + NP * TC_BK * 2
+                                    : (PASSES > 1 ? 2 : 1) * (TcGeo<NP>::A_TILE + TcGeo<NP>::B_TILE);
   const size_t smem = 2 * STAGE + 128;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // 1) W' image
-  {
-    const int64_t nchunks = (2 * g.K + TC_BK - 1) / TC_BK, nsplit = (g.N + NP / 2 - 1) / (NP / 2);
-    const int64_t items = nsplit * nchunks * (NP / 2) * (TC_BK / 4);
-    const int grid = (int)((items + 255) / 256 < 4 * sms ? (items + 255) / 256 : 4 * sms);
-    wimg_kernel<NP, PASSES><<<grid, 256, 0, s>>>(g, reinterpret_cast<uint8_t*>(g.wimg));
-    ++g_launches;
-  }
-  // 2) contraction
-  cudaError_t e =
-      cudaFuncSetAttribute(cgemm_tc_img_kernel<NP, PASSES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  const int sms = device_sms();
+  cudaError_t e;
+  if (!g.wimg_ready && (e = build_wimg_t<NP, PASSES>(g, g.wimg, s)) != cudaSuccess) return e;
+  auto kern = PASSES == 0 ? cgemm_tc_bf16_img_kernel<NP> : cgemm_tc_img_kernel<NP, (PASSES == 0 ? 1 : PASSES)>;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
   const int64_t tiles = ((g.M + TC_BM - 1) / TC_BM) * ((g.N + NP / 2 - 1) / (NP / 2)) * g.batch;
   const int grid = (int)(tiles < sms ? tiles : sms);
-  cgemm_tc_img_kernel<NP, PASSES><<<grid, 256, smem, s>>>(g);
+  kern<<<grid, 256, smem, s>>>(g);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -744,7 +946,12 @@ bool cgemm_tc_supported(const GemmArgs& g) {
 cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s) {
   if (!cgemm_tc_supported(g)) return cudaErrorNotSupported;
   const int np = (int)(2 * g.N);
-  if (passes == 0) {  // BF16 operands
+  if (passes == 0 && g.wimg && (uintptr_t)g.wimg % 16 == 0) {  // BF16 on the W' image
+    if (np <= 64) return launch_tc_img_t<64, 0>(g, s);
+    if (np <= 128) return launch_tc_img_t<128, 0>(g, s);
+    return launch_tc_img_t<256, 0>(g, s);
+  }
+  if (passes == 0) {  // BF16 operands, W' converted per CTA
     if (np <= 64) return launch_tc_bf16_t<64>(g, s);
     if (np <= 128) return launch_tc_bf16_t<128>(g, s);
     return launch_tc_bf16_t<256>(g, s);

@@ -91,6 +91,28 @@ __device__ __forceinline__ void cmac_s(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(a.y, b.x, acc.y);
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+// loop-invariant twiddle with its companion (-b.y, b.x) precomputed: a * b is one
+// FMUL2 + one FFMA2 (built per use, the companion costs a MOV + an FADD)
+struct twp {
+  float2 b, c;
+};
+__device__ __forceinline__ twp make_twp(float2 b) { return twp{b, make_float2(-b.y, b.x)}; }
+__device__ __forceinline__ float2 cmul_p(float2 a, const twp& t) {
+#ifndef TFNO_SCALAR_COMPLEX
+  return fma2(make_float2(a.y, a.y), t.c, mul2(make_float2(a.x, a.x), t.b));
+#else
+  return cmul(a, t.b);
+#endif
+}
+// a * (wr + i wi) for a compile-time constant: swap(a) * (-wi, wi) + a * wr
+// (the swap is an operand modifier, wr a broadcast immediate)
+__device__ __forceinline__ float2 cmul_k(float2 a, float wr, float wi) {
+#ifndef TFNO_SCALAR_COMPLEX
+  return fma2(make_float2(a.y, a.x), make_float2(-wi, wi), mul2(a, make_float2(wr, wr)));
+#else
+  return cmul(a, make_float2(wr, wi));
+#endif
+}
 // multiply by -i (forward, DIR = -1) or +i (inverse, DIR = +1)
 template <int DIR>
 __device__ __forceinline__ float2 mul_dir_i(float2 a) {
@@ -167,15 +189,15 @@ __device__ __forceinline__ void dft16(float2* v) {
 #pragma unroll
   for (int n1 = 0; n1 < 4; ++n1) dft4<DIR>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
   // Y[n1][k1] now at v[n1 + 4 k1]; twiddle w16^{n1 k1}
-  v[1 + 4] = cmul(v[1 + 4], make_float2(c1, d * s1));     // w^1
-  v[1 + 8] = cmul(v[1 + 8], make_float2(r2, d * r2));     // w^2
-  v[1 + 12] = cmul(v[1 + 12], make_float2(s1, d * c1));   // w^3
-  v[2 + 4] = cmul(v[2 + 4], make_float2(r2, d * r2));     // w^2
+  v[1 + 4] = cmul_k(v[1 + 4], c1, d * s1);     // w^1
+  v[1 + 8] = cmul_k(v[1 + 8], r2, d * r2);     // w^2
+  v[1 + 12] = cmul_k(v[1 + 12], s1, d * c1);   // w^3
+  v[2 + 4] = cmul_k(v[2 + 4], r2, d * r2);     // w^2
   v[2 + 8] = mul_dir_i<DIR>(v[2 + 8]);                    // w^4 = DIR i
-  v[2 + 12] = cmul(v[2 + 12], make_float2(-r2, d * r2));  // w^6
-  v[3 + 4] = cmul(v[3 + 4], make_float2(s1, d * c1));     // w^3
-  v[3 + 8] = cmul(v[3 + 8], make_float2(-r2, d * r2));    // w^6
-  v[3 + 12] = cmul(v[3 + 12], make_float2(-c1, -d * s1)); // w^9
+  v[2 + 12] = cmul_k(v[2 + 12], -r2, d * r2);  // w^6
+  v[3 + 4] = cmul_k(v[3 + 4], s1, d * c1);     // w^3
+  v[3 + 8] = cmul_k(v[3 + 8], -r2, d * r2);    // w^6
+  v[3 + 12] = cmul_k(v[3 + 12], -c1, -d * s1); // w^9
   float2 o[16];
 #pragma unroll
   for (int k1 = 0; k1 < 4; ++k1) {
@@ -263,19 +285,19 @@ __device__ __forceinline__ void dft16_in(float2* v) {
     dft4_in<DIR, NIN / 4>(v[3], v[7], v[11], v[15]);
     constexpr int N1 = NIN < 4 ? NIN : 4;  // nonzero n1 rows
     if constexpr (N1 > 1) {
-      v[1 + 4] = cmul(v[1 + 4], make_float2(c1, d * s1));
-      v[1 + 8] = cmul(v[1 + 8], make_float2(r2, d * r2));
-      v[1 + 12] = cmul(v[1 + 12], make_float2(s1, d * c1));
+      v[1 + 4] = cmul_k(v[1 + 4], c1, d * s1);
+      v[1 + 8] = cmul_k(v[1 + 8], r2, d * r2);
+      v[1 + 12] = cmul_k(v[1 + 12], s1, d * c1);
     }
     if constexpr (N1 > 2) {
-      v[2 + 4] = cmul(v[2 + 4], make_float2(r2, d * r2));
+      v[2 + 4] = cmul_k(v[2 + 4], r2, d * r2);
       v[2 + 8] = mul_dir_i<DIR>(v[2 + 8]);
-      v[2 + 12] = cmul(v[2 + 12], make_float2(-r2, d * r2));
+      v[2 + 12] = cmul_k(v[2 + 12], -r2, d * r2);
     }
     if constexpr (N1 > 3) {
-      v[3 + 4] = cmul(v[3 + 4], make_float2(s1, d * c1));
-      v[3 + 8] = cmul(v[3 + 8], make_float2(-r2, d * r2));
-      v[3 + 12] = cmul(v[3 + 12], make_float2(-c1, -d * s1));
+      v[3 + 4] = cmul_k(v[3 + 4], s1, d * c1);
+      v[3 + 8] = cmul_k(v[3 + 8], -r2, d * r2);
+      v[3 + 12] = cmul_k(v[3 + 12], -c1, -d * s1);
     }
     float2 o[16];
 #pragma unroll

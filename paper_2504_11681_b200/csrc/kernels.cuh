@@ -33,6 +33,7 @@ struct GemmArgs {
   float alpha;
   int64_t fold;  // batch elements folded into one M tile (0/1 = none; mode-layout fast path only)
   void* wimg;    // tcgen05 paths: caller scratch for the real-embedded W' image (nullptr: build per CTA)
+  int wimg_ready;  // wimg already holds the image of W (tfno_prepare_weights): skip the build launch
 };
 
 // Row-fused layer kernel (FFT along contiguous rows -> CGEMM over the
@@ -67,6 +68,8 @@ bool cgemm_tc_supported(const GemmArgs& g);
 cudaError_t launch_cgemm_tc(const GemmArgs& g, int passes, cudaStream_t s);
 // bytes of the W' image (TF32 / 3xTF32) for an N x K channel mix; 0 for other precisions
 size_t cgemm_tc_wimg_bytes(int64_t N, int64_t K, int prec);
+// build the W' image of g.W (precision 1 TF32, 2 BF16, 3 3xTF32) into img
+cudaError_t build_cgemm_wimg(const GemmArgs& g, int prec, void* img, cudaStream_t s);
 // precision dispatch: 0 FP32 SIMT, 1 TF32 tcgen05, 2 BF16 tcgen05, 3 3xTF32 tcgen05
 // (launch_cgemm_tc passes: 1 TF32, 3 3xTF32, 0 BF16)
 inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s) {

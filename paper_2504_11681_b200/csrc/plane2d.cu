@@ -699,7 +699,9 @@ static int plane_mix(const tfno_cfg* c) {
   if (!plane2d_tuned(c)) return 3;
   const int env = plane_generic_env();
   if (env >= 0) return env & 3;
-  return c->dim_x == 512 ? 1 : 0;
+  // measured (profiles/r02/plane_mix_a.txt): generic forward wins at 512^2 / 64 (C4 6.60 -> 6.23 ms)
+  // and 256^2 / 16 (C5 layer 1.75 -> 1.68 ms); the tuned inverses and the 256^2 / 32 forward stay
+  return (c->dim_x == 512 || c->keep_x == 16) && c->dim_x != 128 ? 1 : 0;
 }
 
 cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw,
@@ -717,8 +719,8 @@ cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y
 }
 
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
-                                 float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t st,
-                                 void (*mark)(cudaStream_t)) {
+                                 float2* Cm, const float2* tw, int prec, void* wimg, int wimg_ready,
+                                 cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
   const int mix = plane_mix(c);
   const bool nat = mix != 0;  // the generic kernels use the natural mode order; the tuned pair its own
@@ -730,6 +732,7 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
   GemmArgs ga{MQ, N, H, B, A, 1, MQ, H * MQ, w, N, 1, 0, Cm, 1, MQ, N * MQ,
               (float)(1.0 / ((double)c->dim_x * c->dim_y))};
   ga.wimg = wimg;
+  ga.wimg_ready = wimg_ready;
   if ((e = launch_cgemm_prec(ga, prec, st)) != cudaSuccess) return e;
   if (mark) mark(st);
   e = (mix & 2) ? plane_g_run(c, 1, Cm, y, B * N, tw, 1.0f, st) : tuned_inv(c, Cm, y, B * N, tw, 1.0f, nat, st);

@@ -12,8 +12,8 @@ int64_t plane2d_modes(const tfno_cfg* c);
 bool plane2d_spectrum_ok(const tfno_cfg* c);
 int plane_g_kp(const tfno_cfg* c);
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
-                                 float2* Cm, const float2* tw, int prec, void* wimg, cudaStream_t s,
-                                 void (*mark)(cudaStream_t));
+                                 float2* Cm, const float2* tw, int prec, void* wimg, int wimg_ready,
+                                 cudaStream_t s, void (*mark)(cudaStream_t));
 // natural-order mode tensors [planes][kx][ky] (spectrum API); inverse scaled by `scale`
 cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw, cudaStream_t s);
 cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y, float scale, const float2* tw,

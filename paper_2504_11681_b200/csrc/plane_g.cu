@@ -1,7 +1,7 @@
 // Launchers for the generic per-plane 2D kernels (plane_g.cuh): one
 // instantiation per (dy, KP) with dy in {64 ... 1024}, KP in {8 ... 128}.
-// Each translation unit compiles the dy values listed in PLANE_G_DYS so the
-// build parallelises; plane_g_dispatch.cu routes a config to the right unit.
+// The build compiles this file once per row length (-DPLANE_G_DY=64 ... 1024)
+// so the units compile in parallel; plane2d.cu routes a config to its unit.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,18 +28,24 @@ struct PGCfg {
   static constexpr bool BIG = KP >= 128;  // accumulate classes in global, mode tile read from L2
   using GF = PG<DY, KP, KP, NTHF>;
   using GI = PG<DY, KP, KP, NTHI>;
+  // forward accumulators in shared memory when they fit next to everything else (frees registers
+  // for the hoisted twiddle companions; 1024 keeps registers)
+  static constexpr size_t FWD_BASE = sizeof(float2) * ((size_t)S * GF::TEAMS * DY + (size_t)GF::NTB * GF::TB +
+                                                       (size_t)KP * KP + DY + KP + 1024) + 16 * S + 16;
+  static constexpr size_t ACC_BYTES = sizeof(float2) * (size_t)GF::TASKS2 * GF::KA * GF::NTH;
+  static constexpr bool ACCS = !BIG && FWD_BASE + ACC_BYTES <= 227 * 1024;
 };
 
 template <class G>
-size_t g_fwd_smem(int S, int dx) {
-  return sizeof(float2) * ((size_t)S * G::TEAMS * G::DY + 2 * (size_t)G::TB + (size_t)G::KXP * G::KYP + G::DY +
-                           G::KXP + dx) +
+size_t g_fwd_smem(int S, bool accs, int dx) {
+  return sizeof(float2) * ((size_t)S * G::TEAMS * G::DY + (size_t)G::NTB * G::TB + (size_t)G::KXP * G::KYP +
+                           (accs ? (size_t)G::TASKS2 * G::KA * G::NTH : 0) + G::DY + G::KXP + dx) +
          16 * S + 16;
 }
 template <class G>
 size_t g_inv_smem(bool cing, int dx) {
-  return sizeof(float2) * ((cing ? 0 : (size_t)G::KXP * G::KYP) + (size_t)G::KXP * G::KYP + 2 * (size_t)G::TB +
-                           G::DY + G::KXP + dx) +
+  return sizeof(float2) * ((cing ? 0 : (size_t)G::KXP * G::KYP) + (size_t)G::KXP * G::KYP +
+                           (size_t)G::NTB * G::TB + G::DY + G::KXP + dx) +
          16;
 }
 
@@ -61,8 +67,8 @@ cudaError_t g_fwd(const float2* x, float2* A, int64_t planes, int dx, int kx, in
   using C = PGCfg<DY, KP>;
   using G = typename C::GF;
   if (planes <= 0) return cudaSuccess;
-  auto kern = plane_fwd_g<G, C::S, C::BIG>;
-  const size_t smem = g_fwd_smem<G>(C::S, dx);
+  auto kern = plane_fwd_g<G, C::S, C::BIG, C::ACCS>;
+  const size_t smem = g_fwd_smem<G>(C::S, C::ACCS, dx);
   int grid = 0;
   cudaError_t e = persistent_grid(kern, G::NTH + 32, smem, planes, &grid);
   if (e != cudaSuccess) return e;

@@ -41,6 +41,9 @@ struct PG {
   static constexpr int TB = TEAMS * V * TS;
   static constexpr int TASKS2 = (8 * KYP + NTH - 1) / NTH;
   static constexpr int F = T >= A ? T / A : 1;  // kept bins per lane after the reduce
+  // transpose buffers: a team of <= 32 threads syncs with __syncwarp, so one
+  // buffer + a second (free) team sync; 2-warp teams double-buffer instead
+  static constexpr int NTB = M <= 32 ? 1 : 2;
   static_assert(A >= 1 && M == A * V, "row geometry");
   static_assert(NTH % M == 0 && TEAMS >= 1 && KXP % TEAMS == 0, "teams");
   static_assert(KXP >= 8 && KA <= 16 && KYP <= DY && KYP >= 1, "keep");
@@ -81,7 +84,9 @@ __device__ __forceinline__ void lane_reduce(float2* v, int a, int& off) {
 
 // ============================================================== forward
 // x[plane] (dx*DY) -> A[plane][KXP][KYP] (natural order, masked to kx x ky)
-template <class G, int S, bool ACCG>
+// ACCG: large keeps accumulate the classes in the output tile (L2); else the
+// per-thread accumulators live in shared memory (ACCS) or registers
+template <class G, int S, bool ACCG, bool ACCS>
 __global__ void __launch_bounds__(G::NTH + 32, 1)
     plane_fwd_g(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes, int dx, int kx, int ky,
                 const float2* __restrict__ twg) {
@@ -89,9 +94,10 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   constexpr int KXP = G::KXP, KYP = G::KYP, KA = G::KA, IPC = G::IPC, TS = G::TS, NTH = G::NTH, F = G::F;
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);  // S x TEAMS x DY
-  float2* tb = ring + S * TEAMS * DY;              // 2 x TB (double-buffered transpose)
-  float2* Tc = tb + 2 * G::TB;                     // KXP x KYP class buffer
-  float2* twy = Tc + KXP * KYP;                    // w_DY^k
+  float2* tb = ring + S * TEAMS * DY;              // NTB x TB transpose buffers
+  float2* Tc = tb + G::NTB * G::TB;                // KXP x KYP class buffer
+  float2* accs = Tc + KXP * KYP;                   // ACCS: TASKS2 x KA x NTH accumulators
+  float2* twy = accs + (ACCS ? G::TASKS2 * KA * NTH : 0);  // w_DY^k
   float2* twk = twy + DY;                          // w_KXP^k
   float2* twx = twk + KXP;                         // w_dx^k
   uint64_t* full = reinterpret_cast<uint64_t*>(twx + dx);
@@ -143,17 +149,18 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   // ---------------- compute threads
   const int team = tid / M, tt = tid % M;
   const int r_ = tt / A, a_ = tt % A;
-  float2 tw1[V];
+  twp tw1[V];
 #pragma unroll
-  for (int r = 0; r < V; ++r) tw1[r] = twy[r * tt];
-  float2 tw3[T];
+  for (int r = 0; r < V; ++r) tw1[r] = make_twp(twy[r * tt]);
+  twp tw3[T];
 #pragma unroll
-  for (int k = 0; k < T; ++k) tw3[k] = twy[(V * k * a_) % DY];
+  for (int k = 0; k < T; ++k) tw3[k] = make_twp(twy[(V * k * a_) % DY]);
   // stage-2 output validity: lanes holding a kept bin after the reduce
   const bool st_ok = (r_ < RN) && (T >= A || (a_ % (A / (T < A ? T : A))) == 0);
 
-  float2 acc[ACCG ? 1 : G::TASKS2][ACCG ? 1 : KA];
-  if constexpr (!ACCG) {
+  constexpr bool ACCR = !ACCG && !ACCS;  // register accumulators
+  float2 acc[ACCR ? G::TASKS2 : 1][ACCR ? KA : 1];
+  if constexpr (ACCR) {
 #pragma unroll
     for (int a = 0; a < G::TASKS2; ++a)
 #pragma unroll
@@ -171,6 +178,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
       for (int j = 0; j < IPC; ++j) {
         mbar_wait(&full[slot], phase);
         float2* tbt = tb + buf * G::TB + team * V * TS;
+        if (G::NTB == 1 && j > 0) gteam_sync<M>(team);  // previous row's stage 2 is done with tbt
         // ---- stage 1: V-point DFT over y2, twiddle w_DY^{r tt}, transpose
         {
           float2 v[V];
@@ -181,7 +189,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
           if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
           dft<V, -1>(v);
 #pragma unroll
-          for (int r = 1; r < V; ++r) v[r] = cmul(v[r], tw1[r]);
+          for (int r = 1; r < V; ++r) v[r] = cmul_p(v[r], tw1[r]);
 #pragma unroll
           for (int r = 0; r < RN; ++r) tbt[r * TS + tt] = v[r];
         }
@@ -203,7 +211,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
           } else {
             dft<V, -1>(u);
 #pragma unroll
-            for (int k = 0; k < T; ++k) vals[k] = (A > 1 && k > 0) ? cmul(u[k % V], tw3[k]) : u[k % V];
+            for (int k = 0; k < T; ++k) vals[k] = (A > 1 && k > 0) ? cmul_p(u[k % V], tw3[k]) : u[k % V];
           }
           int off = 0;
           lane_reduce<T, A / 2>(vals, a_, off);
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
             for (int i = 0; i < F; ++i) Tc[x1 * KYP + r_ + V * (off + i)] = vals[i];
           }
         }
-        buf ^= 1;
+        if (G::NTB == 2) buf ^= 1;
         if (++slot == S) {
           slot = 0;
           phase ^= 1u;
@@ -261,6 +269,19 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
                 *d = o;
               }
             }
+          } else if constexpr (ACCS) {
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+              float2* ap = accs + (jj * KA + u) * NTH + tid;
+              float2 o = x0 == 0 ? make_float2(0.f, 0.f) : *ap;
+              cmac(o, w[u], twx[(s2 + 8 * u) * x0]);
+              if (x0 == R - 1) {
+                const int p = s2 + 8 * u;
+                dstA[p * KYP + q] = (p < kx && q < ky) ? o : make_float2(0.f, 0.f);
+              } else {
+                *ap = o;
+              }
+            }
           } else {
 #pragma unroll
             for (int u = 0; u < KA; ++u) cmac(acc[jj][u], w[u], twx[(s2 + 8 * u) * x0]);
@@ -268,7 +289,7 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
         }
       }
       named_bar(kGComputeBar, NTH);
-      if constexpr (!ACCG) {
+      if constexpr (ACCR) {
         if (x0 == R - 1) {
 #pragma unroll
           for (int jj = 0; jj < G::TASKS2; ++jj) {
@@ -301,8 +322,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   float2* cin = reinterpret_cast<float2*>(smem);  // KXP x KYP (TMA target; unused if CING)
   float2* Gb = cin + (CING ? 0 : KXP * KYP);      // KXP x KYP
-  float2* tb = Gb + KXP * KYP;                    // 2 x TB
-  float2* twy = tb + 2 * G::TB;                   // conj w_DY^k
+  float2* tb = Gb + KXP * KYP;                    // NTB x TB
+  float2* twy = tb + G::NTB * G::TB;              // conj w_DY^k
   float2* twk = twy + DY;                         // conj w_KXP^k
   float2* twx = twk + KXP;                        // scale * conj w_dx^k
   uint64_t* bar = reinterpret_cast<uint64_t*>(twx + dx);
@@ -329,11 +350,11 @@ __global__ void __launch_bounds__(G::NTH, 1)
   };
   if (!CING && tid == 0 && nmine > 0) issue(0);
 
-  float2 tw1[V], tw3[T];
+  twp tw1[V], tw3[T];
 #pragma unroll
-  for (int r = 0; r < V; ++r) tw1[r] = twy[r * tt];
+  for (int r = 0; r < V; ++r) tw1[r] = make_twp(twy[r * tt]);
 #pragma unroll
-  for (int k = 0; k < T; ++k) tw3[k] = twy[(V * k * a_) % DY];
+  for (int k = 0; k < T; ++k) tw3[k] = make_twp(twy[(V * k * a_) % DY]);
   int buf = 0;
   for (int64_t k = 0; k < nmine; ++k) {
     const int64_t pl = blockIdx.x + k * gridDim.x;
@@ -375,6 +396,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
       for (int j = 0; j < IPC; ++j) {
         const int x1 = j * TEAMS + team;
         float2* tbt = tb + buf * G::TB + team * V * TS;
+        if (G::NTB == 1 && j > 0) gteam_sync<M>(team);  // previous row's stage B is done with tbt
         // ---- stage A: (r, a) -- bins r + V*k (k < T), twiddle w_M^{+k a}, V-point iDFT over k
         if (r_ < RN) {
           float2 u[V];
@@ -383,7 +405,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
           for (int k = 0; k < T; ++k) {
             float2 g = Gb[x1 * KYP + r_ + V * k];
-            if (A > 1 && k > 0) g = cmul(g, tw3[k]);
+            if (A > 1 && k > 0) g = cmul_p(g, tw3[k]);
             u[k % V] = (k < V) ? g : cadd(u[k % V], g);
           }
           dft_in<V, 1, (T < V ? T : V)>(u);
@@ -397,13 +419,13 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
           for (int r = 0; r < V; ++r) v[r] = r < RN ? tbt[r * TS + tt] : make_float2(0.f, 0.f);
 #pragma unroll
-          for (int r = 1; r < RN; ++r) v[r] = cmul(v[r], tw1[r]);
+          for (int r = 1; r < RN; ++r) v[r] = cmul_p(v[r], tw1[r]);
           dft_in<V, 1, RN>(v);
           float2* orow = yp + (int64_t)(x0 + R * x1) * DY;
 #pragma unroll
           for (int y2 = 0; y2 < V; ++y2) __stcs(orow + tt + M * y2, v[y2]);
         }
-        buf ^= 1;
+        if (G::NTB == 2) buf ^= 1;
       }
     }
   }

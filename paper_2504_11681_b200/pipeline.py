@@ -201,9 +201,34 @@ def layer_schedule(cfg: FnoLayerConfig, mode: str = "fully_fused", precision: st
     return int(n), buf.value.decode()
 
 
+class PackedWeights:
+    """The tcgen05 contraction's real-embedded W' image of one weight tensor
+    (tfno_prepare_weights): built once, reused by every run_layer_device call
+    with ``packed=`` (no per-call image build launch)."""
+
+    def __init__(self, cfg: FnoLayerConfig, w, precision: str, stream=None):
+        t = _device.torch()
+        if precision not in ("tf32", "tf32x3", "bf16"):
+            raise FnofuseError(f"packed weights are for the tensor-core precisions, not {precision!r}")
+        w = w if (w.dtype == t.complex64 and w.is_contiguous()) else w.to(t.complex64).contiguous()
+        c = cfg_struct(cfg)
+        self.precision, self.hidden_dim, self.output_dim = precision, cfg.hidden_dim, cfg.output_dim
+        nbytes = int(lib().tfno_packed_weight_bytes(ctypes.byref(c), PREC_CODES[precision]))
+        self.data = t.empty(max(nbytes, 16), dtype=t.uint8, device=w.device)
+        self.w = w
+        check(lib().tfno_prepare_weights(ctypes.byref(c), PREC_CODES[precision], w.data_ptr(), self.data.data_ptr(),
+                                         _device.stream_ptr(stream)), "tfno_prepare_weights")
+
+
+def prepare_weights(cfg: FnoLayerConfig, w, precision: str = "tf32x3", stream=None) -> PackedWeights:
+    """Pack W[H][N] (complex64 CUDA tensor, row-major) for the tensor-core
+    contraction once per weight tensor (SURVEY.md §8b tfno_prepare_weights)."""
+    return PackedWeights(cfg, w, precision, stream)
+
+
 def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILES, mode: str = "fully_fused",
                      fft_batch_size: int = FFT_BLOCK_BATCH, out=None, precision: str = "fp32", stream=None,
-                     validate: bool = True, workspace=None):
+                     validate: bool = True, workspace=None, packed: "PackedWeights" = None):
     """Device API: x [B,H,dx,dy] and w [H,N] complex64 CUDA tensors (w in
     row-major [H][N]); returns the [B,N,dx,dy] CUDA tensor.  Asynchronous
     on ``stream`` (default: torch's current stream).  ``workspace``: an
@@ -237,10 +262,20 @@ def run_layer_device(cfg: FnoLayerConfig, x, w, tiles: TileConfig = DEFAULT_TILE
         ws = workspace if nbytes else None
     else:
         ws = _device.workspace(nbytes, dev, stream)  # per (device, stream): no sharing across streams
-    rc = lib().tfno_layer_forward(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                  ws.data_ptr() if ws is not None else None, nbytes,
-                                  _device.stream_ptr(stream))
-    check(rc, "tfno_layer_forward")
+    if packed is not None and precision != "fp32":
+        if (packed.precision != precision or packed.hidden_dim != cfg.hidden_dim
+                or packed.output_dim != cfg.output_dim):
+            raise FnofuseError("packed weights were prepared for another precision or shape")
+        rc = lib().tfno_layer_forward_packed(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(),
+                                             packed.data.data_ptr(), out.data_ptr(),
+                                             ws.data_ptr() if ws is not None else None, nbytes,
+                                             _device.stream_ptr(stream))
+        check(rc, "tfno_layer_forward_packed")
+    else:
+        rc = lib().tfno_layer_forward(ctypes.byref(c), mcode, pcode, x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                      ws.data_ptr() if ws is not None else None, nbytes,
+                                      _device.stream_ptr(stream))
+        check(rc, "tfno_layer_forward")
     if user_out is not None:
         if stream is not None:
             with t.cuda.stream(stream):

@@ -58,6 +58,32 @@ def test_full_size_batch_slices_vs_oracle(env, name, shape, idx):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("name,shape,idx", [
+    ("C4", (128, 128, 128, 512, 512, 64, 64, 2), (0, 127)),
+    ("C5-layer", (256, 64, 64, 256, 256, 16, 16, 2), (0, 255)),
+])
+def test_full_size_tensorcore_precisions(env, name, shape, idx):
+    """The tcgen05 contraction variants at full C4 / C5-layer size, batch slices vs
+    the oracle at the stated tolerances (3xTF32 1e-5, TF32 1e-3, BF16 5e-3)."""
+    from types import SimpleNamespace
+    T, O, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x = _rand(torch, (cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), 31)
+    w = _rand(torch, (cfg.hidden_dim, cfg.output_dim), 32).contiguous()
+    wh = w.cpu().numpy()
+    c1 = SimpleNamespace(**{**cfg.__dict__, "batch": 1})
+    refs = {b: O.run_layer_values(c1, x[b:b + 1].cpu().numpy(), wh) for b in idx}
+    for prec, tol in (("tf32x3", 1e-5), ("tf32", 1e-3), ("bf16", 5e-3)):
+        y = T.run_layer_device(cfg, x, w, precision=prec)
+        torch.cuda.synchronize()
+        for b in idx:
+            err = T.max_rel_error(y[b:b + 1].cpu().numpy(), refs[b])
+            assert err < tol, (name, prec, b, err)
+        del y
+    del x
+    torch.cuda.empty_cache()
+
+
 def test_c4_linearity_and_shards(env):
     """C4 layer shape (batch 16): L(x1 + 2 x2) == L(x1) + 2 L(x2) and two
     batch shards == the whole batch (bitwise)."""

@@ -45,3 +45,26 @@ def test_layer_tensorcore_precisions(env, shape):
         for prec, tol in (("tf32x3", 1e-5), ("tf32", 1e-3), ("bf16", 5e-3)):
             y = T.run_layer_device(cfg, xd, wd, mode=mode, precision=prec)
             assert T.max_rel_error(y.cpu().numpy(), ref) < tol, (mode, prec)
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 8, 512, 512, 64, 64, 2), (3, 12, 20, 1, 1024, 1, 128, 1),
+                                   (2, 16, 8, 128, 256, 40, 24, 2)])
+@pytest.mark.parametrize("prec", ["tf32x3", "tf32", "bf16"])
+def test_prepared_weights_match_per_call_image(env, shape, prec):
+    """tfno_prepare_weights (W' image built once per weight tensor) gives the same
+    layer bitwise as the per-call image build, with one launch fewer."""
+    T, O, torch = env
+    cfg = T.FnoLayerConfig(*shape)
+    x, w = O.random_inputs(cfg, 9)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    mode = "fully_fused" if cfg.rank == 2 else "fft_optimized"
+    y0 = T.run_layer_device(cfg, xd, wd, mode=mode, precision=prec).clone()
+    pw = T.prepare_weights(cfg, wd, prec)
+    n0 = T._lib.lib().tfno_launch_count()
+    y1 = T.run_layer_device(cfg, xd, wd, mode=mode, precision=prec, packed=pw)
+    n1 = T._lib.lib().tfno_launch_count() - n0
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    assert n1 == T.layer_schedule(cfg, mode, prec)[0] - 1  # no image-build launch
+    with pytest.raises(T.FnofuseError):
+        T.run_layer_device(cfg, xd, wd, mode=mode, precision="tf32" if prec != "tf32" else "bf16", packed=pw)

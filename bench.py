@@ -142,6 +142,8 @@ def stage_algorithmic_bytes(cfg, desc):
         "x-ifft": B * N * kx * dy + B * N * dx * dy,
         "plane-fft2d": B * H * dx * dy + B * H * kx * ky,
         "plane-ifft2d": B * N * kx * ky + B * N * dx * dy,
+        # channel mix fused into the inverse: A in, W, y out (C stays in the L2 ring)
+        "plane-mix-ifft2d": B * H * kx * ky + H * N + B * N * dx * dy,
     }
     return [(name, E * t.get(name, 0)) for name in desc.split("|")]
 

@@ -173,8 +173,13 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
   if (g.rank == 2 && mode == TFNO_FULLY_FUSED && plane2d_supported(c)) {
     s.plane2d = true;
     s.need_A = s.need_C = true;
-    s.launches = 3;
-    s.desc = "plane-fft2d|cgemm-modes|plane-ifft2d";
+    if (plane2d_fusedmix(c, prec)) {
+      s.launches = 2;
+      s.desc = "plane-fft2d|plane-mix-ifft2d";
+    } else {
+      s.launches = 3;
+      s.desc = "plane-fft2d|cgemm-modes|plane-ifft2d";
+    }
     return s;
   }
   FusedArgs fa{};
@@ -405,7 +410,7 @@ size_t base_ws_bytes(const tfno_cfg* c, int mode, int prec) {  // intermediates 
   if (s.need_mid) e += g.B * g.N * g.kx * g.dy;
   const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;  // generic plane kernels: KP^2 padded modes
   if (s.need_A) e += g.B * g.H * mq;
-  if (s.need_C) e += g.B * g.N * mq;
+  if (s.need_C) e += s.plane2d ? plane2d_c_elems(c, prec) : g.B * g.N * mq;
   return e * sizeof(float2);
 }
 
@@ -708,7 +713,7 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
   if (s.need_mid) { mid = p; p += g.B * g.N * g.kx * g.dy; }
   const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;
   if (s.need_A) { A = p; p += g.B * g.H * mq; }
-  if (s.need_C) { Cm = p; p += g.B * g.N * mq; }
+  if (s.need_C) { Cm = p; p += s.plane2d ? plane2d_c_elems(c, prec) : g.B * g.N * mq; }
   // W' image: the caller's packed weights (tfno_prepare_weights) or built per call in the workspace tail
   const int wimg_ready = (packed && wimg_need) ? 1 : 0;
   void* wimg = wimg_ready ? const_cast<void*>(packed)

@@ -654,6 +654,81 @@ cudaError_t plane_g_run_256(int, int, const float2*, float2*, int64_t, int, int,
 cudaError_t plane_g_run_512(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
 cudaError_t plane_g_run_1024(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
 
+size_t plane_g_invmix_smem_64(int, int, int);
+size_t plane_g_invmix_smem_128(int, int, int);
+size_t plane_g_invmix_smem_256(int, int, int);
+size_t plane_g_invmix_smem_512(int, int, int);
+size_t plane_g_invmix_smem_1024(int, int, int);
+cudaError_t plane_g_invmix_run_64(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
+                                  const float2*, float, cudaStream_t);
+cudaError_t plane_g_invmix_run_128(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
+                                   const float2*, float, cudaStream_t);
+cudaError_t plane_g_invmix_run_256(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
+                                   const float2*, float, cudaStream_t);
+cudaError_t plane_g_invmix_run_512(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
+                                   const float2*, float, cudaStream_t);
+cudaError_t plane_g_invmix_run_1024(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
+                                    const float2*, float, cudaStream_t);
+
+static size_t plane_g_invmix_smem(const tfno_cfg* c) {
+  const int kp = plane_g_kp(c);
+  if (!kp || c->hidden_dim > 4096) return 0;
+  const int H = c->hidden_dim, dx = c->dim_x;
+  switch (c->dim_y) {
+    case 64: return plane_g_invmix_smem_64(kp, H, dx);
+    case 128: return plane_g_invmix_smem_128(kp, H, dx);
+    case 256: return plane_g_invmix_smem_256(kp, H, dx);
+    case 512: return plane_g_invmix_smem_512(kp, H, dx);
+    case 1024: return plane_g_invmix_smem_1024(kp, H, dx);
+    default: return 0;
+  }
+}
+
+static cudaError_t plane_g_invmix_run(const tfno_cfg* c, const float2* A, const float2* w, float2* Cs, float2* y,
+                                      const float2* tw, float alpha, cudaStream_t st) {
+  const int kp = plane_g_kp(c);
+  const int B = c->batch, H = c->hidden_dim, N = c->output_dim, dx = c->dim_x;
+  switch (c->dim_y) {
+    case 64: return plane_g_invmix_run_64(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 128: return plane_g_invmix_run_128(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 256: return plane_g_invmix_run_256(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 512: return plane_g_invmix_run_512(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 1024: return plane_g_invmix_run_1024(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+constexpr int kMixGNHost = 8;  // == kMixGN in plane_g.cu (output channels per fused-mix task)
+static int plane_fusedmix_env() {  // TFNO_PLANE_FUSEDMIX=0/1 overrides the per-geometry default (A/B)
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFNO_PLANE_FUSEDMIX");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+bool plane2d_fusedmix(const tfno_cfg* c, int prec) {
+  if (prec != TFNO_FP32 || !plane2d_supported(c)) return false;
+  if ((int64_t)c->batch * ((c->output_dim + 7) / 8) > (1LL << 40)) return false;
+  const int env = plane_fusedmix_env();
+  if (env == 0 || plane_g_invmix_smem(c) == 0) return false;
+  if (env == 1) return true;
+  // default: where the standalone contraction is a large share of the layer and
+  // every CTA has enough tasks to hide the first task's mix (the prologue) --
+  // measured (profiles/r02/fusedmix_ab*.txt): C4 (H = N = 128, 13.8 tasks per
+  // CTA) 7.81 -> 7.43 ms for mix + inverse; C3 / C5 (H = N = 64, <= 1.7 tasks
+  // per CTA at C3) lose 0.22 -> 0.31 ms / 1.56 -> 1.91 ms
+  const int64_t tasks = (int64_t)c->batch * ((c->output_dim + kMixGNHost - 1) / kMixGNHost);
+  return (int64_t)c->hidden_dim * c->output_dim >= 128 * 128 && tasks >= 8LL * device_sms();
+}
+
+int64_t plane2d_c_elems(const tfno_cfg* c, int prec) {
+  const int64_t mq = plane2d_modes(c);
+  if (plane2d_fusedmix(c, prec)) return (int64_t)device_sms() * 2 * kMixGNHost * mq;
+  return (int64_t)c->batch * c->output_dim * mq;
+}
+
 static cudaError_t plane_g_run(const tfno_cfg* c, int dir, const float2* in, float2* out, int64_t planes,
                                const float2* tw, float scale, cudaStream_t st) {
   const int kp = plane_g_kp(c);
@@ -699,9 +774,10 @@ static int plane_mix(const tfno_cfg* c) {
   if (!plane2d_tuned(c)) return 3;
   const int env = plane_generic_env();
   if (env >= 0) return env & 3;
-  // measured (profiles/r02/plane_mix_a.txt): generic forward wins at 512^2 / 64 (C4 6.60 -> 6.23 ms)
-  // and 256^2 / 16 (C5 layer 1.75 -> 1.68 ms); the tuned inverses and the 256^2 / 32 forward stay
-  return (c->dim_x == 512 || c->keep_x == 16) && c->dim_x != 128 ? 1 : 0;
+  // measured, same box (profiles/r02/ab_r1.txt, mix_c5.txt): at 512^2 / 64 both generic kernels
+  // (C4 13.80-13.89 ms vs 14.12-14.13 tuned and 14.11-14.18 for generic forward + tuned inverse, whose
+  // natural-order tile reads conflict); the tuned pair elsewhere (C3 0.460 vs 0.474-0.484, C5L 3.14 vs 3.18-3.60)
+  return c->dim_x == 512 && c->dim_y == 512 && c->keep_x == 64 ? 3 : 0;
 }
 
 cudaError_t launch_plane2d_fwd(const tfno_cfg* c, const float2* x, float2* modes, const float2* tw,
@@ -723,6 +799,18 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
                                  cudaStream_t st, void (*mark)(cudaStream_t)) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
   const int mix = plane_mix(c);
+  if (plane2d_fusedmix(c, prec)) {
+    // forward in the natural mode order the generic inverse reads, then the
+    // channel mix + inverse in one kernel (C stays in the per-CTA L2 ring Cm)
+    cudaError_t e = (mix & 1) ? plane_g_run(c, -1, x, A, B * H, tw, 1.0f, st) : tuned_fwd(c, x, A, B * H, tw, true, st);
+    if (e != cudaSuccess) return e;
+    if (mark) mark(st);
+    if ((e = plane_g_invmix_run(c, A, w, Cm, y, tw, (float)(1.0 / ((double)c->dim_x * c->dim_y)), st)) !=
+        cudaSuccess)
+      return e;
+    if (mark) mark(st);
+    return cudaSuccess;
+  }
   const bool nat = mix != 0;  // the generic kernels use the natural mode order; the tuned pair its own
   cudaError_t e = (mix & 1) ? plane_g_run(c, -1, x, A, B * H, tw, 1.0f, st) : tuned_fwd(c, x, A, B * H, tw, nat, st);
   if (e != cudaSuccess) return e;

@@ -431,4 +431,275 @@ __global__ void __launch_bounds__(G::NTH, 1)
   }
 }
 
+// ============================================================== inverse + channel mix
+// One kernel for the second half of the rank-2 layer (N1: the contraction is
+// no longer a pass of its own).  Work unit = task (b, n0 .. n0+GN-1):
+//   mix warps (the last 4 warps): C[b, n0+g, m] = alpha * sum_h A[b, h, m] W[h, n0+g]
+//     in FP32 SIMT (packed FFMA2, h ascending like cgemm.gemm_kloop,
+//     cgemm.py:83-95).  A[b, h0:h0+HC, m0:m0+MC] chunks stream into a shared
+//     ring with TMA bulk copies (afull / aempty mbarriers); the W columns of
+//     the task sit in shared memory as (wr, wi, -wi, wr).  The task's C planes
+//     go to a per-CTA two-slot ring in global memory (L2-resident, it is read
+//     back within one task) -- one task ahead of the inverse warps.
+//   inverse warps (the first NTH threads): plane_inv_g's padded 2D inverse of
+//     each plane of the task, its mode tile TMA-loaded from the ring slot once
+//     the mix warps have published it (cready) and the slot handed back
+//     (cfree) when the last plane's tile has landed.
+// The mode tensor A therefore makes one HBM round trip (written by the
+// forward, read here) and C never leaves L2 in steady state; the reference
+// keeps C on chip the same way (pipeline.py:185-206, 245-250).
+constexpr int kMixThreads = 128;  // 4 mix warps
+constexpr int kMixBar = 14;       // named barrier of the mix warps
+
+template <int MQ>
+struct MixGeo {
+  static constexpr int MC = MQ < 512 ? MQ : 512;  // modes per chunk (128 * MI)
+  static constexpr int MI = MC / 128;              // modes per mix thread
+  static constexpr int HC = 2048 / MC;             // hidden channels per chunk (16 KiB chunks)
+  static constexpr int SA_MAX = 8;                 // ring depth: as many chunks as shared memory allows
+  static_assert(MC % 128 == 0 && MQ % MC == 0, "mode chunking");
+};
+
+template <class G, int GN>
+__global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
+    plane_invmix_g(const float2* __restrict__ Ain, const float2* __restrict__ W, float2* __restrict__ Cs,
+                   float2* __restrict__ y, int B, int H, int N, int dx, const float2* __restrict__ twg,
+                   float alpha, int SA) {
+  constexpr int DY = G::DY, V = G::V, M = G::M, A = G::A, T = G::T, RN = G::RN, TEAMS = G::TEAMS;
+  constexpr int KXP = G::KXP, KYP = G::KYP, KA = G::KA, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
+  constexpr int MQ = KXP * KYP;
+  using X = MixGeo<MQ>;
+  constexpr int MC = X::MC, MI = X::MI, HC = X::HC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* ring = reinterpret_cast<float2*>(smem);          // SA x HC x MC (TMA targets)
+  float4* Wt = reinterpret_cast<float4*>(ring + SA * HC * MC);  // H x GN packed W columns
+  float2* cin = reinterpret_cast<float2*>(Wt + (size_t)H * GN);  // MQ (TMA target)
+  float2* Gb = cin + MQ;                                   // MQ
+  float2* tb = Gb + MQ;                                    // NTB x TB
+  float2* twy = tb + G::NTB * G::TB;
+  float2* twk = twy + DY;
+  float2* twx = twk + KXP;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(twx + dx);   // cin landed
+  uint64_t* cready = bar + 1;                              // [2] C slot written (128 arrivals)
+  uint64_t* cfree = cready + 2;                            // [2] C slot read back (1 arrival)
+  uint64_t* afull = cfree + 2;                             // [SA_MAX]
+  uint64_t* aempty = afull + X::SA_MAX;                    // [SA_MAX] (4 warp arrivals)
+
+  const int tid = threadIdx.x;
+  const int R = dx / KXP;
+  const int NG = (N + GN - 1) / GN;
+  const int64_t tasks = (int64_t)B * NG;
+  const int64_t nmine = tasks > blockIdx.x ? (tasks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  float2* myC = Cs + (int64_t)blockIdx.x * 2 * GN * MQ;  // this CTA's two task slots
+
+  for (int k = tid; k < DY; k += blockDim.x) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]));
+  for (int k = tid; k < KXP; k += blockDim.x) twk[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / KXP)]));
+  for (int k = tid; k < dx; k += blockDim.x) twx[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / dx)]));
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&cready[s], kMixThreads);
+      mbar_init(&cfree[s], 1);
+    }
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], kMixThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= NTH) {
+    // ================= mix warps
+    const int ct = tid - NTH;
+    constexpr int NMB = MQ / MC;
+    const int NHC = (H + HC - 1) / HC;
+    const int64_t per_task = (int64_t)NMB * NHC;
+    const int64_t nch = nmine * per_task;
+    const uint64_t pol_a = policy_evict_last();  // A[b] is read by the NG tasks of batch b
+    auto issue_chunk = [&](int64_t c, int slot) {
+      const int64_t k = c / per_task;
+      const int r = (int)(c - k * per_task), mb = r / NHC, hc = r % NHC;
+      const int64_t b = (blockIdx.x + k * gridDim.x) / NG;
+      const int h0 = hc * HC, hn = min(HC, H - h0);
+      mbar_expect_tx(&afull[slot], (uint32_t)(hn * MC * 8));
+      const float2* src = Ain + ((b * H + h0) * (int64_t)MQ + (int64_t)mb * MC);
+      for (int kk = 0; kk < hn; ++kk)
+        tma_load_1d(ring + (slot * HC + kk) * MC, src + (int64_t)kk * MQ, MC * 8, &afull[slot], pol_a);
+    };
+    if (ct == 0)
+      for (int64_t c = 0; c < SA && c < nch; ++c) issue_chunk(c, (int)c);
+    int64_t c = 0;
+    int aslot = 0;
+    uint32_t aphase = 0;
+    for (int64_t k = 0; k < nmine; ++k) {
+      const int64_t t = blockIdx.x + k * gridDim.x;
+      const int n0 = (int)(t % NG) * GN;
+      const int gn = min(GN, N - n0);
+      named_bar(kMixBar, kMixThreads);  // all mix warps are done with the previous task's Wt
+      for (int i = ct; i < H * GN; i += kMixThreads) {
+        const int h = i / GN, g = i % GN;
+        const float2 w = (g < gn) ? __ldg(&W[(int64_t)h * N + n0 + g]) : make_float2(0.f, 0.f);
+        Wt[i] = make_float4(w.x, w.y, -w.y, w.x);
+      }
+      named_bar(kMixBar, kMixThreads);
+      const int s = (int)(k & 1);
+      if (k >= 2) mbar_wait(&cfree[s], (uint32_t)(((k >> 1) - 1) & 1));  // the inverse has read slot s back
+      float2* cdst = myC + (int64_t)s * GN * MQ;
+#pragma unroll 1
+      for (int mb = 0; mb < NMB; ++mb) {
+        float2 acc[MI][GN];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int g = 0; g < GN; ++g) acc[i][g] = make_float2(0.f, 0.f);
+#pragma unroll 1
+        for (int hc = 0; hc < NHC; ++hc, ++c) {
+          const int slot = aslot;
+          mbar_wait(&afull[slot], aphase);
+          const float2* As = ring + slot * HC * MC + ct;
+          const float4* wt = Wt + hc * HC * GN;
+          const int hn = min(HC, H - hc * HC);
+#pragma unroll 2
+          for (int kk = 0; kk < hn; ++kk) {
+            float2 a[MI];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[i] = As[kk * MC + 128 * i];
+#pragma unroll
+            for (int g = 0; g < GN; ++g) {
+              const float4 w = wt[kk * GN + g];
+#pragma unroll
+              for (int i = 0; i < MI; ++i) {
+                acc[i][g] = fma2(make_float2(a[i].x, a[i].x), make_float2(w.x, w.y), acc[i][g]);
+                acc[i][g] = fma2(make_float2(a[i].y, a[i].y), make_float2(w.z, w.w), acc[i][g]);
+              }
+            }
+          }
+          __syncwarp();
+          if ((ct & 31) == 0) mbar_arrive(&aempty[slot]);
+          if (ct == 0 && c + SA < nch) {  // refill the slot once all four mix warps are done with it
+            mbar_wait(&aempty[slot], aphase);
+            issue_chunk(c + SA, slot);
+          }
+          if (++aslot == SA) {
+            aslot = 0;
+            aphase ^= 1u;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GN; ++g)
+          if (g < gn)
+#pragma unroll
+            for (int i = 0; i < MI; ++i) cdst[(int64_t)g * MQ + mb * MC + ct + 128 * i] = cscale(acc[i][g], alpha);
+      }
+      fence_proxy_async_global();  // the C tile is read back with cp.async.bulk
+      mbar_arrive(&cready[s]);
+    }
+    return;
+  }
+
+  // ================= inverse warps (plane_inv_g per plane of each task)
+  const int team = tid / M, tt = tid % M;
+  const int r_ = tt / A, a_ = tt % A;
+  const uint64_t pol = policy_evict_first();
+  auto task_gn = [&](int64_t k) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    return min(GN, N - (int)(t % NG) * GN);
+  };
+  // tid 0: mode tile of plane g of task k -> cin (waits for the slot to be published)
+  auto issue = [&](int64_t k, int g) {
+    const int s = (int)(k & 1);
+    if (g == 0) mbar_wait(&cready[s], (uint32_t)((k >> 1) & 1));
+    mbar_expect_tx(bar, MQ * 8);
+    tma_load_1d(cin, myC + ((int64_t)s * GN + g) * MQ, MQ * 8, bar, pol);
+  };
+  if (tid == 0 && nmine > 0) issue(0, 0);
+
+  twp tw1[V], tw3[T];
+#pragma unroll
+  for (int r = 0; r < V; ++r) tw1[r] = make_twp(twy[r * tt]);
+#pragma unroll
+  for (int k = 0; k < T; ++k) tw3[k] = make_twp(twy[(V * k * a_) % DY]);
+  int buf = 0;
+  uint32_t pc = 0;  // planes done (cin phase)
+  for (int64_t k = 0; k < nmine; ++k) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int64_t b = t / NG;
+    const int n0 = (int)(t % NG) * GN;
+    const int gn = min(GN, N - n0);
+    for (int g = 0; g < gn; ++g, ++pc) {
+      mbar_wait(bar, pc & 1u);
+      if (tid == 0 && g == gn - 1) mbar_arrive(&cfree[k & 1]);  // slot fully read back
+      float2* yp = y + (b * N + n0 + g) * (int64_t)dx * DY;
+      for (int x0 = 0; x0 < R; ++x0) {
+        named_bar(kGComputeBar, NTH);  // previous class's rows are done with Gb
+        for (int tau = tid; tau < 8 * KYP; tau += NTH) {
+          const int q = tau % KYP, s2 = tau / KYP;
+          float2 w[KA];
+#pragma unroll
+          for (int u = 0; u < KA; ++u) {
+            const int p = s2 + 8 * u;
+            w[u] = cmul(cin[p * KYP + q], twx[p * x0]);
+          }
+          dft<KA, 1>(w);
+#pragma unroll
+          for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twk[s2 * i]);
+#pragma unroll
+          for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KYP + q] = w[i];
+        }
+        named_bar(kGComputeBar, NTH);
+        if (x0 == R - 1 && tid == 0) {  // cin fully consumed: next plane's tile
+          if (g + 1 < gn)
+            issue(k, g + 1);
+          else if (k + 1 < nmine)
+            issue(k + 1, 0);
+        }
+        for (int tau = tid; tau < KA * KYP; tau += NTH) {
+          const int q = tau % KYP, i = tau / KYP;
+          float2 v[8];
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) v[s2] = Gb[(s2 * KA + i) * KYP + q];
+          dft8<1>(v);
+#pragma unroll
+          for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KYP + q] = v[m];
+        }
+        named_bar(kGComputeBar, NTH);
+#pragma unroll 1
+        for (int j = 0; j < IPC; ++j) {
+          const int x1 = j * TEAMS + team;
+          float2* tbt = tb + buf * G::TB + team * V * TS;
+          if (G::NTB == 1 && j > 0) gteam_sync<M>(team);
+          if (r_ < RN) {
+            float2 u[V];
+#pragma unroll
+            for (int c = 0; c < V; ++c) u[c] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int kb = 0; kb < T; ++kb) {
+              float2 gv = Gb[x1 * KYP + r_ + V * kb];
+              if (A > 1 && kb > 0) gv = cmul_p(gv, tw3[kb]);
+              u[kb % V] = (kb < V) ? gv : cadd(u[kb % V], gv);
+            }
+            dft_in<V, 1, (T < V ? T : V)>(u);
+#pragma unroll
+            for (int c = 0; c < V; ++c) tbt[r_ * TS + a_ + A * c] = u[c];
+          }
+          gteam_sync<M>(team);
+          {
+            float2 v[V];
+#pragma unroll
+            for (int r = 0; r < V; ++r) v[r] = r < RN ? tbt[r * TS + tt] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 1; r < RN; ++r) v[r] = cmul_p(v[r], tw1[r]);
+            dft_in<V, 1, RN>(v);
+            float2* orow = yp + (int64_t)(x0 + R * x1) * DY;
+#pragma unroll
+            for (int y2 = 0; y2 < V; ++y2) __stcs(orow + tt + M * y2, v[y2]);
+          }
+          if (G::NTB == 2) buf ^= 1;
+        }
+      }
+    }
+  }
+}
+
 }  // namespace tfno

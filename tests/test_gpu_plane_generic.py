@@ -16,7 +16,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-5
-PLANE = "plane-fft2d|cgemm-modes|plane-ifft2d"
+# FP32 default: channel mix fused into the inverse; TFNO_PLANE_FUSEDMIX=0 keeps the standalone CGEMM
+PLANES = ("plane-fft2d|plane-mix-ifft2d", "plane-fft2d|cgemm-modes|plane-ifft2d")
 
 # (B, H, N, dx, dy, kx, ky)
 SHAPES = [
@@ -76,7 +77,7 @@ def _ids(s):
 def test_generic_plane_layer(T, O, shape):
     B, H, N, dx, dy, kx, ky = shape
     cfg = T.FnoLayerConfig(B, H, N, dx, dy, kx, ky, rank=2)
-    assert T.layer_schedule(cfg, "fully_fused", "fp32")[1] == PLANE, shape
+    assert T.layer_schedule(cfg, "fully_fused", "fp32")[1] in PLANES, shape
     x, w = O.random_inputs(cfg, 1000 + sum(shape))
     out, led = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
     exact = O.reference_layer(cfg, x, w)
@@ -124,6 +125,43 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, TFNO_PLANE_GENERIC=mix, PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+_FUSEDMIX_CODE = r"""
+import numpy as np, paper_2504_11681_b200 as T
+from oracle import fnofuse_port as O
+FM = "@FM@"
+want = "plane-fft2d|plane-mix-ifft2d" if FM == "1" else "plane-fft2d|cgemm-modes|plane-ifft2d"
+for s in [(2, 3, 13, 512, 512, 64, 64), (64, 8, 64, 64, 64, 16, 16), (40, 21, 19, 128, 128, 32, 32),
+          (3, 70, 9, 256, 128, 20, 12), (2, 5, 8, 64, 512, 16, 16), (1, 300, 17, 128, 64, 16, 16),
+          (2, 2, 3, 256, 256, 16, 16), (600, 2, 5, 64, 64, 8, 8)]:
+    cfg = T.FnoLayerConfig(*s, rank=2)
+    d = T.layer_schedule(cfg, "fully_fused")[1]
+    kp = max(8, 1 << (max(s[5], s[6]) - 1).bit_length())
+    assert d == want or kp not in (16, 32, 64), (s, d)
+    x, w = O.random_inputs(cfg, 7 + s[0])
+    out, _ = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
+    err = T.max_rel_error(out.data, O.reference_layer(cfg, x, w))
+    assert err < 1e-5, (s, err)
+    b, _ = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
+    assert np.array_equal(out.data, b.data), s
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("fusedmix", ["0", "1"])
+def test_fused_mix_inverse(fusedmix):
+    """plane_invmix_g (channel mix inside the inverse kernel, C in a per-CTA
+    two-task ring) and the standalone-CGEMM schedule: ragged N (tasks of 8
+    output channels), H not a multiple of the A chunk, more tasks than CTAs
+    (the C ring and the A ring wrap many times), every fused KP (16/32/64),
+    non-square planes, the C4 plane shape; FP32 bar vs the float64
+    composition, bitwise determinism."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TFNO_PLANE_FUSEDMIX=fusedmix, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _FUSEDMIX_CODE.replace("@FM@", fusedmix)], env=env,
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 

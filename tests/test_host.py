@@ -108,8 +108,12 @@ def test_native_violations_match_python():
 
 def test_schedules_and_workspace():
     c4 = T.FnoLayerConfig(128, 128, 128, 512, 512, 64, 64, 2)
-    assert T.layer_schedule(c4, "fully_fused") == (3, "plane-fft2d|cgemm-modes|plane-ifft2d")
-    assert T.workspace_bytes(c4, "fully_fused") == 2 * 128 * 128 * 64 * 64 * 8
+    # FP32: the channel mix runs inside the inverse kernel (plane_invmix_g), its C
+    # tiles in a per-CTA two-task ring (SMs x 2 x 8 planes; 148 SMs without a device)
+    assert T.layer_schedule(c4, "fully_fused") == (2, "plane-fft2d|plane-mix-ifft2d")
+    assert T.workspace_bytes(c4, "fully_fused") == (128 * 128 + 148 * 2 * 8) * 64 * 64 * 8
+    # tensor-core contractions keep the standalone tcgen05 CGEMM between the plane kernels
+    assert T.layer_schedule(c4, "fully_fused", "tf32x3")[1] == "plane-fft2d|cgemm-modes|plane-ifft2d"
     c1 = T.FnoLayerConfig(16, 64, 64, 1, 128, 1, 32, 1)
     assert T.layer_schedule(c1, "fully_fused") == (1, "fused1d-fft-cgemm-ifft")  # one launch (fused1d.cu)
     assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused-fft-cgemm|y-ifft")
@@ -123,6 +127,8 @@ def test_schedules_and_workspace():
     # ragged keeps pad to KP = 32 modes per axis in the A / C workspace tensors
     r3 = T.FnoLayerConfig(2, 16, 8, 256, 128, 20, 12, 2)
     assert T.workspace_bytes(r3, "fully_fused") == 2 * (16 + 8) * 32 * 32 * 8
+    c3 = T.FnoLayerConfig(32, 64, 64, 256, 256, 32, 32, 2)  # too few mix tasks per CTA: standalone CGEMM
+    assert T.layer_schedule(c3, "fully_fused") == (3, "plane-fft2d|cgemm-modes|plane-ifft2d")
     r4 = T.FnoLayerConfig(2, 16, 16, 64, 32, 8, 16, 2)  # dy < 64: the paper schedule
     assert T.layer_schedule(r4, "fully_fused") == (3, "x-fft|fused-fft-cgemm-ifft|x-ifft")
     f = T.layer_flops(c4)

@@ -295,6 +295,15 @@ size_t staged_ws(const Geo& g) {
   return (size_t)(bc * g.H * g.dx * g.dy + g.B * g.H * g.kx * g.ky + g.B * g.N * g.kx * g.ky) * 8;
 }
 
+// cuBLAS handles and cuFFT plans are created on first use per stream; when that
+// first use happens while the stream is being captured into a CUDA graph, their
+// (uncaptured) setup allocations run in relaxed capture mode for this thread
+struct RelaxedCapture {
+  cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&m); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&m); }
+};
+
 int get_plan(int dev, int rank, int dx, int dy, int64_t batch, cudaStream_t st, cufftHandle* out) {
   auto key = std::make_tuple(rank, dx, dy, batch, st);
   auto& ctx = g_base[dev];
@@ -303,6 +312,7 @@ int get_plan(int dev, int rank, int dx, int dy, int64_t batch, cudaStream_t st, 
     *out = it->second;
     return 0;
   }
+  RelaxedCapture relax;
   cufftHandle h;
   if (cufftCreate(&h) != CUFFT_SUCCESS) return TFNO_ECUFFT;
   size_t wsz = 0;
@@ -335,11 +345,15 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
   auto& ctx = g_base[dev];
   cublasHandle_t& blas = ctx.blas[st];
   if (!blas) {
+    RelaxedCapture relax;
     if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) {
       ctx.blas.erase(st);
       return TFNO_ECUBLAS;
     }
     cublasSetMathMode(blas, CUBLAS_DEFAULT_MATH);  // true FP32, no TF32
+    // a per-handle workspace allocated here, so no GEMM allocates lazily (inside a capture)
+    void* bws = nullptr;
+    if (cudaMalloc(&bws, 32u << 20) == cudaSuccess) cublasSetWorkspace(blas, bws, 32u << 20);
   }
   const int64_t bc = staged_chunk(g);
   float2* full = ws;

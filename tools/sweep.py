@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 import paper_2504_11681_b200 as T  # noqa: E402
+from oracle import fnofuse_port as O  # noqa: E402  (checker only: parity per sweep point)
 
 
 def timeit(fn, reps, warm=3):
@@ -89,10 +90,26 @@ def main():
         best_base = min(row["staged"], row["torch_fft"])
         row["best_ours_fp32"] = ours
         row["speedup_vs_best_unfused"] = round(best_base / ours, 3)
+        row["speedup_vs_staged"] = {m: round(row["staged"] / row[m], 3) for m in T.MODES if m != "staged"}
         row["frac_measured_hbm"] = round(fl["bytes"] / (ours * 1e-3) / 6543.4e9, 4)
+        t_roof = max(fl["bytes"] / 8.0e12, fl["flops"] / 74.4e12)  # SURVEY.md §8d layer roofline
+        row["frac_layer_roofline"] = round(t_roof / (ours * 1e-3), 4)
+        # parity per point (north_star: max relative error reported per config): every mode on a
+        # batch slice against the CPU oracle (bitwise equal to fnofuse.run_layer)
+        nb = min(B, 2 if rk == 2 else 4)
+        cs = T.FnoLayerConfig(nb, H, N, dx, dy, kx, ky, rk)
+        xs = x[:nb].cpu().numpy()
+        ref = O.run_layer_values(cs, xs, w.cpu().numpy())
+        errs = {}
+        for mode in T.MODES:
+            ys = T.run_layer_device(cs, x[:nb].contiguous(), w, mode=mode)
+            errs[mode] = float(T.max_rel_error(ys.cpu().numpy(), ref))
+        row["max_rel_error"] = errs
+        row["parity_sample"] = f"batch[0:{nb}] vs oracle port (fnofuse.run_layer semantics)"
         rows.append(row)
-        print(json.dumps({k: row[k] for k in ("workload", "fully_fused", "best_ours_fp32", "staged", "torch_fft",
-                                              "speedup_vs_best_unfused", "frac_measured_hbm")}), flush=True)
+        print(json.dumps({k: row[k] for k in ("workload", "fully_fused", "fully_fused_schedule", "best_ours_fp32",
+                                              "staged", "speedup_vs_staged", "frac_layer_roofline",
+                                              "frac_measured_hbm", "max_rel_error")}), flush=True)
         del x, w, y
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

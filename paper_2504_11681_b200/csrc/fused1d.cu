@@ -205,6 +205,10 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   }
   __syncthreads();
   if constexpr (CS > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
+  // PDL: the prologue above (barriers, twiddle tables) overlapped the previous layer's tail;
+  // x / W / y are touched only after it has completed
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (tid >= G::NFT + G::NGT) {
     // ================= producer warpgroup (one elected thread issues)
@@ -538,7 +542,18 @@ static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
     const int64_t items = a.G * (a.nsplit > 1 ? a.nsplit : 1);
     const int grid = (int)(items < sms ? items : sms);
     if (grid < 1) return cudaSuccess;
-    kern<<<grid, G::NTH, smem, s>>>(a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(G::NTH);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaSuccess) return e;
   } else {
     const int64_t units = a.G < sms / CS ? a.G : sms / CS;
     if (units < 1) return cudaSuccess;
@@ -547,13 +562,15 @@ static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
     cfg.blockDim = dim3(G::NTH);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess) return e;
   }

@@ -23,6 +23,7 @@
 
 #include "fft_engine.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace tfno {
 
@@ -38,6 +39,15 @@ int device_sms() {
     cache[dev] = n;
   }
   return cache[dev];
+}
+
+bool pdl_enabled(int level) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFNO_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v >= level;
 }
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -194,6 +204,8 @@ __global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kerne
   constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 || PK ? 8 : 16);
   __shared__ __align__(16) float2 As[2][FBK][FBM];
   __shared__ __align__(16) float2 Ws[2][FBK][FBN * (PK ? 2 : 1)];
+  pdl_wait();  // PDL launch: A is the previous kernel's output
+  pdl_launch_dependents();
   const int tid = threadIdx.x;
   const int tm = tid % 16, tn = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.x * FBM, n0 = (int64_t)blockIdx.y * FBN;
@@ -514,9 +526,9 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
     if (g3)
       wide ? launch3m<4, 8>(grid, f, s) : launch3m<8, 4>(grid, f, s);
     else if (wide)
-      cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(f);
+      launch_pdl(cgemm_modes_kernel<4, 8>, grid, dim3(256), 0, s, f);
     else
-      cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(f);
+      launch_pdl(cgemm_modes_kernel<8, 4>, grid, dim3(256), 0, s, f);
   } else if (fast && g.N > 64 && g3) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     launch3m<4, 8>(grid, g, s);
@@ -526,15 +538,15 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   } else if (fast && g.N > 64 && g.M >= 128 && big_tiles()) {
     dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     if (gemm_packed())
-      cgemm_modes_kernel<8, 8, true><<<grid, 256, 0, s>>>(g);
+      launch_pdl(cgemm_modes_kernel<8, 8, true>, grid, dim3(256), 0, s, g);
     else
-      cgemm_modes_kernel<8, 8><<<grid, 256, 0, s>>>(g);
+      launch_pdl(cgemm_modes_kernel<8, 8>, grid, dim3(256), 0, s, g);
   } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
-    cgemm_modes_kernel<4, 8><<<grid, 256, 0, s>>>(g);  // packed form spills at 2 CTAs/SM
+    launch_pdl(cgemm_modes_kernel<4, 8>, grid, dim3(256), 0, s, g);  // packed form spills at 2 CTAs/SM
   } else if (fast && g.M >= 128) {
     dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
-    cgemm_modes_kernel<8, 4><<<grid, 256, 0, s>>>(g);
+    launch_pdl(cgemm_modes_kernel<8, 4>, grid, dim3(256), 0, s, g);
   } else {
     dim3 grid((unsigned)((g.M + GBM - 1) / GBM), (unsigned)((g.N + GBN - 1) / GBN), (unsigned)g.batch);
     cgemm_kernel<<<grid, 256, 0, s>>>(g);

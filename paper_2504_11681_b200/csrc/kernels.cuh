@@ -100,6 +100,28 @@ cudaError_t launch_pad_truncate(const float2* src, int64_t planes, int sx, int s
                                 float scale, cudaStream_t s);
 
 extern thread_local long long g_launches;  // our kernels launched by this thread
-int device_sms();  // SM count of the current device (cached per device)
+int device_sms();
+// programmatic dependent launch (TFNO_PDL: 0 off, 1 = the fused 1D layer kernel only (default),
+// 2 = also the plane / mode-CGEMM kernels).  Measured (profiles/r02/pdl_ab.txt): C1 graph
+// replay 13.5-15.3 -> 12.4 us with it; the 2D kernels gain nothing eagerly (C3, C4) and the
+// C5 4-layer graph slows 12.9 -> 20.7 ms with PDL edges between the plane kernels.
+bool pdl_enabled(int level = 1);
+// launch with the programmatic-stream-serialization attribute: ONLY for kernels
+// that call pdl_wait() (ptx.cuh) before touching memory an earlier kernel writes
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {  // the level-2 kernels (plane / mode CGEMM)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(2) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}  // SM count of the current device (cached per device)
 
 }  // namespace tfno

@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();  // x is read (A written) only once the previous kernel has completed
+  pdl_launch_dependents();
 
   if (tid >= NTH) {
     // ---------------- producer warp: stream the plane rows, class by class
@@ -370,6 +372,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t pol = policy_evict_first();
   auto issue = [&](int64_t k) {
     const int64_t pl = blockIdx.x + k * gridDim.x;
@@ -519,7 +523,8 @@ static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, cons
   cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, NAT, DLD>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  plane_fwd2d_kernel<G, S, NAT, DLD><<<grid, G::NTH + 32, smem, st>>>(x, A, planes, tw);
+  e = launch_pdl(plane_fwd2d_kernel<G, S, NAT, DLD>, dim3(grid), dim3(G::NTH + 32), smem, st, x, A, planes, tw);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }
@@ -548,7 +553,8 @@ static cudaError_t launch_inv_v(const float2* Cm, float2* y, int64_t planes, con
   cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, NAT, DST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  plane_inv2d_kernel<G, SO, NAT, DST><<<grid, G::NTH, smem, st>>>(Cm, y, planes, tw, scale);
+  e = launch_pdl(plane_inv2d_kernel<G, SO, NAT, DST>, dim3(grid), dim3(G::NTH), smem, st, Cm, y, planes, tw, scale);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }

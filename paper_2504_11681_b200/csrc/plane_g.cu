@@ -72,7 +72,8 @@ cudaError_t g_fwd(const float2* x, float2* A, int64_t planes, int dx, int kx, in
   int grid = 0;
   cudaError_t e = persistent_grid(kern, G::NTH + 32, smem, planes, &grid);
   if (e != cudaSuccess) return e;
-  kern<<<grid, G::NTH + 32, smem, st>>>(x, A, planes, dx, kx, ky, tw);
+  e = launch_pdl(kern, dim3(grid), dim3(G::NTH + 32), smem, st, x, A, planes, dx, kx, ky, tw);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }
@@ -88,7 +89,8 @@ cudaError_t g_inv(const float2* Cm, float2* y, int64_t planes, int dx, const flo
   int grid = 0;
   cudaError_t e = persistent_grid(kern, G::NTH, smem, planes, &grid);
   if (e != cudaSuccess) return e;
-  kern<<<grid, G::NTH, smem, st>>>(Cm, y, planes, dx, tw, scale);
+  e = launch_pdl(kern, dim3(grid), dim3(G::NTH), smem, st, Cm, y, planes, dx, tw, scale);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
 }
@@ -139,7 +141,8 @@ cudaError_t g_invmix(const float2* A, const float2* W, float2* Cs, float2* y, in
     cudaError_t e = persistent_grid(kern, G::NTH + kMixThreads, smem, tasks, &grid);
     if (e != cudaSuccess) return e;
     if (grid > device_sms()) grid = device_sms();  // the C ring is sized for one CTA per SM
-    kern<<<grid, G::NTH + kMixThreads, smem, st>>>(A, W, Cs, y, B, H, N, dx, tw, alpha, sa);
+    e = launch_pdl(kern, dim3(grid), dim3(G::NTH + kMixThreads), smem, st, A, W, Cs, y, B, H, N, dx, tw, alpha, sa);
+    if (e != cudaSuccess) return e;
     ++g_launches;
     return cudaGetLastError();
   }

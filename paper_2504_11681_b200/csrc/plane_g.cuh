@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();  // x is read (A written) only once the previous kernel has completed
+  pdl_launch_dependents();
 
   if (tid >= NTH) {
     // ---------------- producer warp: TEAMS rows per ring slot, class by class
@@ -342,6 +344,8 @@ __global__ void __launch_bounds__(G::NTH, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t pol = policy_evict_first();
   auto issue = [&](int64_t k) {
     const int64_t pl = blockIdx.x + k * gridDim.x;
@@ -508,6 +512,8 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (tid >= NTH) {
     // ================= mix warps

@@ -78,6 +78,15 @@ __device__ __forceinline__ float2 shfl_xor2(float2 v, int m) {
   return make_float2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// griddepcontrol.wait: block until the preceding grid in the stream has completed and its
+// memory is visible (a no-op when the kernel was launched without the PDL attribute);
+// launch_dependents: let the next grid start launching (its CTAs then run their prologue
+// and park in their own wait).  Everything before pdl_wait() may only read data no earlier
+// kernel writes (twiddle tables, parameters).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- sync helpers
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -93,3 +93,68 @@ def test_chain_graph_matches_chained_layers(env):
     assert T.max_rel_error(y, ref) < 1e-5
     y2 = ch.forward(xd).cpu().numpy()
     assert np.array_equal(y, y2)
+
+
+_NCCL_WORKER = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+import paper_2504_11681_b200 as T
+from oracle import fnofuse_port as O
+from paper_2504_11681_b200 import multigpu as MG
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", rank=rank, world_size=world)
+cfg = T.FnoLayerConfig(2, 8, 4 * world, 64, 64, 16, 16, 2)
+x, w = O.random_inputs(cfg, 12)
+ref = O.run_layer_values(cfg, x, w)
+h0, h1 = MG.shard_bounds(cfg.hidden_dim, world, rank)
+xd = torch.from_numpy(x[:, h0:h1].copy()).cuda()
+wd = torch.from_numpy(w[h0:h1].copy()).cuda()
+s = torch.cuda.Stream()  # a non-current stream: partial CGEMM -> NCCL -> inverse ordered on it
+y = MG.hidden_split_forward(cfg, xd, wd, how="all_reduce", stream=s)
+torch.cuda.synchronize()
+assert T.max_rel_error(y.cpu().numpy(), ref) < 1e-5, "all_reduce"
+yb = MG.hidden_split_forward(cfg, xd, wd, how="reduce_scatter", stream=s)  # [N/world, B, dx, dy]
+torch.cuda.synchronize()
+nr = cfg.output_dim // world
+mine = np.transpose(ref[:, rank * nr:(rank + 1) * nr], (1, 0, 2, 3))
+assert T.max_rel_error(yb.cpu().numpy(), mine) < 1e-5, "reduce_scatter"
+dist.barrier()
+dist.destroy_process_group()
+print("ok", rank)
+"""
+
+
+def _run_nccl(world):
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(world):
+        e = dict(os.environ, PYTHONPATH=root, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r),
+                 MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", _NCCL_WORKER], env=e, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (o, err) in zip(procs, outs):
+        assert p.returncode == 0 and "ok" in o, err[-3000:]
+
+
+def test_hidden_split_nccl_single_rank():
+    """The NCCL data plane of the hidden-dimension split (all_reduce and
+    reduce_scatter over a process group on the nccl backend), run as a
+    world-1 group on this GPU: exercises the collective calls and their
+    ordering after the partial CGEMM on a non-current stream."""
+    _run_nccl(1)
+
+
+def test_hidden_split_nccl_two_gpus():
+    """Two ranks on two GPUs over NVLink (skipped on a one-GPU box)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    _run_nccl(2)

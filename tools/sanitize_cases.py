@@ -27,7 +27,9 @@ cases = [((1, 2, 2, 128, 128, 16, 16, 2), ["fully_fused"]),            # plane2d
          ((2, 8, 8, 1, 128, 1, 32, 1), ["fully_fused", "fused_fft_gemm", "fused_gemm_ifft"]),  # CT rows fused
          ((3, 64, 64, 1, 256, 1, 32, 1), ["fully_fused"]),               # fused1d, output-channel split 2
          ((200, 32, 64, 1, 256, 1, 32, 1), ["fully_fused"]),             # fused1d, several items per CTA
-         ((150, 16, 64, 1, 1024, 1, 128, 1), ["fully_fused"])]           # fused1d L = 32
+         ((150, 16, 64, 1, 1024, 1, 128, 1), ["fully_fused"]),           # fused1d L = 32
+         ((3, 20, 19, 256, 256, 32, 32, 2), ["fully_fused"]),            # generic plane / fused mix (TFNO_PLANE_FUSEDMIX=1)
+         ((300, 2, 9, 64, 64, 16, 16, 2), ["fully_fused"])]              # more mix tasks than CTAs (rings wrap)
 for shape, modes in cases:
     cfg = T.FnoLayerConfig(*shape)
     x, w = rnd(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), rnd(cfg.hidden_dim, cfg.output_dim)

@@ -34,16 +34,38 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _deps_mtime() -> float:
-    paths = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    paths += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
+DIGEST = OUT + ".sha256"  # content digest of everything the library is built from
+
+
+def source_digest() -> str:
+    """sha256 over every source / header, this build script, the nvcc version and
+    the A/B build hooks: the library is rebuilt whenever any of them changes
+    (content, not modification times, so a copied tree or a clock skew cannot
+    make build() reuse a stale binary)."""
+    import hashlib
+    h = hashlib.sha256()
+    paths = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC))
+    paths += sorted(os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE))
     paths.append(os.path.abspath(__file__))
-    return max(os.path.getmtime(p) for p in paths)
+    for p in paths:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    try:
+        h.update(subprocess.run([_nvcc(), "--version"], capture_output=True, text=True).stdout.encode())
+    except Exception:  # noqa: BLE001
+        pass
+    for k in ("TFNO_SCALAR_FILES", "TFNO_NVCC_DEFS"):
+        h.update(f"{k}={os.environ.get(k, '')}".encode())
+    return h.hexdigest()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
-        return OUT
+    digest = source_digest()
+    if not force and os.path.exists(OUT) and os.path.exists(DIGEST):
+        with open(DIGEST) as f:
+            if f.read().strip() == digest:
+                return OUT
     os.makedirs(BUILD_DIR, exist_ok=True)
     nvcc = _nvcc()
 
@@ -83,6 +105,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, OUT)
+    with open(DIGEST, "w") as f:
+        f.write(digest + "\n")
     return OUT
 
 

@@ -472,6 +472,8 @@ def run_ours(args):
         "schedule": sched, "launch": "one CUDA graph replay per step" if chain is not None else "eager launches",
         "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "traffic_source": ("committed ncu --set full capture (profiles/traffic.json), not measured in this run"
+                                        if traffic is not None else None),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": sbytes[dom][1],
                      "launch_ms": round(stage_ms[dom], 4),
                      "share_of_step": round(stage_ms[dom] / sum(stage_ms), 4) if sum(stage_ms) else None},
@@ -689,13 +691,13 @@ def run_e2e(T, cfg, x, w, mode, prec, args, barrier, max_over_ranks, stream):
     return {"ms": ms, "unit": "GFLOP/s", "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
             "batch_per_rank": cfg.batch,
             "steps": steps, "api": "paper_2504_11681_b200.pipeline.HostPipeline (pinned host in/out, "
-                                   f"chunk {pipe_chunk(cfg)} batch elems, 3 streams)",
+                                   f"chunk {pipe_chunk(cfg)} batch elems; H2D / layer / D2H streams, 3 buffers)",
             "ms_per_step": round(ms, 2)}
 
 
 def pipe_chunk(cfg):
-    per_b = 8 * cfg.dim_x * cfg.dim_y * (cfg.hidden_dim + cfg.output_dim)
-    return max(1, min(cfg.batch, (2 << 30) // max(per_b, 1)))
+    from paper_2504_11681_b200.pipeline import default_pipe_chunk
+    return default_pipe_chunk(cfg)
 
 
 def main():

@@ -405,33 +405,36 @@ def layer_flops(cfg: FnoLayerConfig, mode: str = "fully_fused") -> dict:
 
 
 class HostPipeline:
-    """End-to-end host-buffer execution: the batch is split into chunks that
-    flow H2D -> layer -> D2H on ``nstreams`` CUDA streams, so PCIe copies in
-    both directions overlap the sm_100a kernels of other chunks.  Inputs and
-    outputs are pinned host tensors; device chunk buffers are allocated once
-    and reused."""
+    """End-to-end host-buffer execution as a three-stage software pipeline over
+    batch chunks: one stream per role -- H2D copies, layer kernels, D2H copies
+    -- and ``nbuf`` device chunk buffers, so the two PCIe directions (separate
+    copy engines) and the sm_100a kernels all run back to back:
+
+        H2D(i)     waits for layer(i - nbuf)  (its input buffer is free again)
+        layer(i)   waits for H2D(i) and D2H(i - nbuf) (its output buffer is free)
+        D2H(i)     waits for layer(i)
+
+    Inputs and outputs are pinned host tensors; device buffers are allocated
+    once and reused.  The default chunk is one batch element up to 512 MiB of
+    in+out per chunk (small chunks shorten the pipeline fill / drain; the layer
+    kernels of a chunk are far shorter than its transfers)."""
 
     def __init__(self, cfg: FnoLayerConfig, mode: str = "fully_fused", precision: str = "fp32",
-                 chunk: int | None = None, nstreams: int = 3, device=None):
+                 chunk: int | None = None, nbuf: int = 3, device=None, nstreams: int | None = None):
         t = _device.torch()
         self.dev = _device.require_cuda(device)
         self.cfg, self.mode, self.precision = cfg, mode, precision
-        per_b = 8 * cfg.dim_x * cfg.dim_y * (cfg.hidden_dim + cfg.output_dim)
-        self.chunk = chunk or max(1, min(cfg.batch, (2 << 30) // max(per_b, 1)))
-        self.nstreams = nstreams
+        self.chunk = chunk or default_pipe_chunk(cfg)
+        self.nbuf = max(2, nstreams or nbuf)
         cc = self.chunk
         self.ccfg = FnoLayerConfig(cc, cfg.hidden_dim, cfg.output_dim, cfg.dim_x, cfg.dim_y,
                                    cfg.keep_x, cfg.keep_y, cfg.rank)
-        self.streams = [t.cuda.Stream(self.dev) for _ in range(nstreams)]
+        self.h2d, self.comp, self.d2h = (t.cuda.Stream(self.dev) for _ in range(3))
         self.xb = [t.empty((cc, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=self.dev)
-                   for _ in range(nstreams)]
+                   for _ in range(self.nbuf)]
         self.yb = [t.empty((cc, cfg.output_dim, cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=self.dev)
-                   for _ in range(nstreams)]
-        self.ws = []
-        for _ in range(nstreams):
-            nb = workspace_bytes(self.ccfg, mode, precision)
-            self.ws.append(t.empty(max(nb, 1), dtype=t.uint8, device=self.dev))
-        self.done = [None] * nstreams
+                   for _ in range(self.nbuf)]
+        self.ws = t.empty(max(workspace_bytes(self.ccfg, mode, precision), 1), dtype=t.uint8, device=self.dev)
 
     def __call__(self, x_host, w, out_host):
         """x_host [B,H,dx,dy] / out_host [B,N,dx,dy]: pinned complex64 CPU
@@ -443,31 +446,52 @@ class HostPipeline:
         w_dev = w.to(self.dev, non_blocking=True).contiguous()
         ready = t.cuda.Event()
         ready.record(cur)
+        for st in (self.h2d, self.comp, self.d2h):
+            st.wait_event(ready)
         c = cfg_struct(self.ccfg)
         mcode, pcode = MODE_CODES[self.mode], PREC_CODES[self.precision]
+        nb_, comp_done, out_done = self.nbuf, [], []
         for i, b0 in enumerate(range(0, cfg.batch, self.chunk)):
-            s = i % self.nstreams
-            st = self.streams[s]
+            k = i % nb_
             nb = min(self.chunk, cfg.batch - b0)
-            with t.cuda.stream(st):
-                st.wait_event(ready)
-                xb, yb = self.xb[s][:nb], self.yb[s][:nb]
+            xb, yb = self.xb[k][:nb], self.yb[k][:nb]
+            with t.cuda.stream(self.h2d):
+                if i >= nb_:
+                    self.h2d.wait_event(comp_done[i - nb_])
                 xb.copy_(x_host[b0:b0 + nb], non_blocking=True)
+                in_done = t.cuda.Event()
+                in_done.record(self.h2d)
+            with t.cuda.stream(self.comp):
+                self.comp.wait_event(in_done)
+                if i >= nb_:
+                    self.comp.wait_event(out_done[i - nb_])
                 if nb == self.chunk:
-                    cc, ccfg = c, self.ccfg
+                    cc = c
                 else:
-                    ccfg = FnoLayerConfig(nb, cfg.hidden_dim, cfg.output_dim, cfg.dim_x, cfg.dim_y,
-                                          cfg.keep_x, cfg.keep_y, cfg.rank)
-                    cc = cfg_struct(ccfg)
-                ws = self.ws[s]
+                    cc = cfg_struct(FnoLayerConfig(nb, cfg.hidden_dim, cfg.output_dim, cfg.dim_x, cfg.dim_y,
+                                                   cfg.keep_x, cfg.keep_y, cfg.rank))
                 rc = lib().tfno_layer_forward(ctypes.byref(cc), mcode, pcode, xb.data_ptr(), w_dev.data_ptr(),
-                                              yb.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+                                              yb.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                              self.comp.cuda_stream)
                 check(rc, "tfno_layer_forward")
+                ev = t.cuda.Event()
+                ev.record(self.comp)
+                comp_done.append(ev)
+            with t.cuda.stream(self.d2h):
+                self.d2h.wait_event(comp_done[i])
                 out_host[b0:b0 + nb].copy_(yb, non_blocking=True)
-        for st in self.streams:
-            cur.wait_stream(st)
+                ev = t.cuda.Event()
+                ev.record(self.d2h)
+                out_done.append(ev)
+        cur.wait_stream(self.d2h)
         cur.synchronize()
         return out_host
+
+
+def default_pipe_chunk(cfg: FnoLayerConfig) -> int:
+    """Batch elements per HostPipeline chunk: up to 512 MiB of input + output."""
+    per_b = 8 * cfg.dim_x * cfg.dim_y * (cfg.hidden_dim + cfg.output_dim)
+    return max(1, min(cfg.batch, (512 << 20) // max(per_b, 1)))
 
 
 def run_layer_host(cfg: FnoLayerConfig, x_host, w, out_host=None, mode: str = "fully_fused",

@@ -691,7 +691,7 @@ def run_e2e(T, cfg, x, w, mode, prec, args, barrier, max_over_ranks, stream):
     return {"ms": ms, "unit": "GFLOP/s", "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
             "batch_per_rank": cfg.batch,
             "steps": steps, "api": "paper_2504_11681_b200.pipeline.HostPipeline (pinned host in/out, "
-                                   f"chunk {pipe_chunk(cfg)} batch elems; H2D / layer / D2H streams, 3 buffers)",
+                                   f"chunk {pipe_chunk(cfg)} batch elems; 2 H2D + 2 D2H copy streams, 1 kernel stream, 4 buffers)",
             "ms_per_step": round(ms, 2)}
 
 

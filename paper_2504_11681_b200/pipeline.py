@@ -406,9 +406,10 @@ def layer_flops(cfg: FnoLayerConfig, mode: str = "fully_fused") -> dict:
 
 class HostPipeline:
     """End-to-end host-buffer execution as a three-stage software pipeline over
-    batch chunks: one stream per role -- H2D copies, layer kernels, D2H copies
-    -- and ``nbuf`` device chunk buffers, so the two PCIe directions (separate
-    copy engines) and the sm_100a kernels all run back to back:
+    batch chunks: streams per role -- ``ncopy`` H2D streams and ``ncopy`` D2H
+    streams (alternating chunks, so each direction keeps more than one copy in
+    flight) and one kernel stream -- over ``nbuf`` device chunk buffers, so the
+    two PCIe directions and the sm_100a kernels all run back to back:
 
         H2D(i)     waits for layer(i - nbuf)  (its input buffer is free again)
         layer(i)   waits for H2D(i) and D2H(i - nbuf) (its output buffer is free)
@@ -420,16 +421,19 @@ class HostPipeline:
     kernels of a chunk are far shorter than its transfers)."""
 
     def __init__(self, cfg: FnoLayerConfig, mode: str = "fully_fused", precision: str = "fp32",
-                 chunk: int | None = None, nbuf: int = 3, device=None, nstreams: int | None = None):
+                 chunk: int | None = None, nbuf: int = 4, ncopy: int = 2, device=None):
         t = _device.torch()
         self.dev = _device.require_cuda(device)
         self.cfg, self.mode, self.precision = cfg, mode, precision
         self.chunk = chunk or default_pipe_chunk(cfg)
-        self.nbuf = max(2, nstreams or nbuf)
+        self.nbuf = max(2, nbuf)
+        self.ncopy = max(1, min(ncopy, self.nbuf))
         cc = self.chunk
         self.ccfg = FnoLayerConfig(cc, cfg.hidden_dim, cfg.output_dim, cfg.dim_x, cfg.dim_y,
                                    cfg.keep_x, cfg.keep_y, cfg.rank)
-        self.h2d, self.comp, self.d2h = (t.cuda.Stream(self.dev) for _ in range(3))
+        self.h2d = [t.cuda.Stream(self.dev) for _ in range(self.ncopy)]
+        self.d2h = [t.cuda.Stream(self.dev) for _ in range(self.ncopy)]
+        self.comp = t.cuda.Stream(self.dev)
         self.xb = [t.empty((cc, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=self.dev)
                    for _ in range(self.nbuf)]
         self.yb = [t.empty((cc, cfg.output_dim, cfg.dim_x, cfg.dim_y), dtype=t.complex64, device=self.dev)
@@ -446,7 +450,7 @@ class HostPipeline:
         w_dev = w.to(self.dev, non_blocking=True).contiguous()
         ready = t.cuda.Event()
         ready.record(cur)
-        for st in (self.h2d, self.comp, self.d2h):
+        for st in self.h2d + self.d2h + [self.comp]:
             st.wait_event(ready)
         c = cfg_struct(self.ccfg)
         mcode, pcode = MODE_CODES[self.mode], PREC_CODES[self.precision]
@@ -455,12 +459,13 @@ class HostPipeline:
             k = i % nb_
             nb = min(self.chunk, cfg.batch - b0)
             xb, yb = self.xb[k][:nb], self.yb[k][:nb]
-            with t.cuda.stream(self.h2d):
+            hs, ds = self.h2d[i % self.ncopy], self.d2h[i % self.ncopy]
+            with t.cuda.stream(hs):
                 if i >= nb_:
-                    self.h2d.wait_event(comp_done[i - nb_])
+                    hs.wait_event(comp_done[i - nb_])
                 xb.copy_(x_host[b0:b0 + nb], non_blocking=True)
                 in_done = t.cuda.Event()
-                in_done.record(self.h2d)
+                in_done.record(hs)
             with t.cuda.stream(self.comp):
                 self.comp.wait_event(in_done)
                 if i >= nb_:
@@ -477,13 +482,14 @@ class HostPipeline:
                 ev = t.cuda.Event()
                 ev.record(self.comp)
                 comp_done.append(ev)
-            with t.cuda.stream(self.d2h):
-                self.d2h.wait_event(comp_done[i])
+            with t.cuda.stream(ds):
+                ds.wait_event(comp_done[i])
                 out_host[b0:b0 + nb].copy_(yb, non_blocking=True)
                 ev = t.cuda.Event()
-                ev.record(self.d2h)
+                ev.record(ds)
                 out_done.append(ev)
-        cur.wait_stream(self.d2h)
+        for st in self.d2h:
+            cur.wait_stream(st)
         cur.synchronize()
         return out_host
 

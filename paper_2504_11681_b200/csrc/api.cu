@@ -150,6 +150,7 @@ cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st
 // schedule decision shared by workspace sizing and the forward
 struct Sched {
   bool staged = false, plane2d = false, rows_fast = false, warp_fused = false, f1 = false;
+  bool plane_mix = false;  // rank-2 plane path with the channel mix fused into the inverse
   int rows_NT = 0, f1_split = 1, f1_cluster = 1;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
@@ -174,6 +175,7 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
     s.plane2d = true;
     s.need_A = s.need_C = true;
     if (plane2d_fusedmix(c, prec)) {
+      s.plane_mix = true;
       s.launches = 2;
       s.desc = "plane-fft2d|plane-mix-ifft2d";
     } else {
@@ -405,7 +407,7 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
 }
 
 // the channel mix runs as a standalone CGEMM (plane2d path or the unfused row schedule)
-bool sched_has_cgemm(const Sched& s) { return s.plane2d || (!s.staged && !s.fg && !s.gi); }
+bool sched_has_cgemm(const Sched& s) { return (s.plane2d && !s.plane_mix) || (!s.plane2d && !s.staged && !s.fg && !s.gi); }
 
 size_t wimg_bytes_for(const tfno_cfg* c, int mode, int prec) {
   Sched s = make_sched(c, mode, prec);

@@ -660,46 +660,46 @@ cudaError_t plane_g_run_256(int, int, const float2*, float2*, int64_t, int, int,
 cudaError_t plane_g_run_512(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
 cudaError_t plane_g_run_1024(int, int, const float2*, float2*, int64_t, int, int, int, const float2*, float, cudaStream_t);
 
-size_t plane_g_invmix_smem_64(int, int, int);
-size_t plane_g_invmix_smem_128(int, int, int);
-size_t plane_g_invmix_smem_256(int, int, int);
-size_t plane_g_invmix_smem_512(int, int, int);
-size_t plane_g_invmix_smem_1024(int, int, int);
+size_t plane_g_invmix_smem_64(int, int, int, int);
+size_t plane_g_invmix_smem_128(int, int, int, int);
+size_t plane_g_invmix_smem_256(int, int, int, int);
+size_t plane_g_invmix_smem_512(int, int, int, int);
+size_t plane_g_invmix_smem_1024(int, int, int, int);
 cudaError_t plane_g_invmix_run_64(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
-                                  const float2*, float, cudaStream_t);
+                                  const float2*, float, int, cudaStream_t);
 cudaError_t plane_g_invmix_run_128(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
-                                   const float2*, float, cudaStream_t);
+                                  const float2*, float, int, cudaStream_t);
 cudaError_t plane_g_invmix_run_256(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
-                                   const float2*, float, cudaStream_t);
+                                  const float2*, float, int, cudaStream_t);
 cudaError_t plane_g_invmix_run_512(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
-                                   const float2*, float, cudaStream_t);
+                                  const float2*, float, int, cudaStream_t);
 cudaError_t plane_g_invmix_run_1024(int, const float2*, const float2*, float2*, float2*, int, int, int, int,
-                                    const float2*, float, cudaStream_t);
+                                  const float2*, float, int, cudaStream_t);
 
-static size_t plane_g_invmix_smem(const tfno_cfg* c) {
+static size_t plane_g_invmix_smem(const tfno_cfg* c, int prec) {
   const int kp = plane_g_kp(c);
   if (!kp || c->hidden_dim > 4096) return 0;
   const int H = c->hidden_dim, dx = c->dim_x;
   switch (c->dim_y) {
-    case 64: return plane_g_invmix_smem_64(kp, H, dx);
-    case 128: return plane_g_invmix_smem_128(kp, H, dx);
-    case 256: return plane_g_invmix_smem_256(kp, H, dx);
-    case 512: return plane_g_invmix_smem_512(kp, H, dx);
-    case 1024: return plane_g_invmix_smem_1024(kp, H, dx);
+    case 64: return plane_g_invmix_smem_64(kp, H, dx, prec);
+    case 128: return plane_g_invmix_smem_128(kp, H, dx, prec);
+    case 256: return plane_g_invmix_smem_256(kp, H, dx, prec);
+    case 512: return plane_g_invmix_smem_512(kp, H, dx, prec);
+    case 1024: return plane_g_invmix_smem_1024(kp, H, dx, prec);
     default: return 0;
   }
 }
 
 static cudaError_t plane_g_invmix_run(const tfno_cfg* c, const float2* A, const float2* w, float2* Cs, float2* y,
-                                      const float2* tw, float alpha, cudaStream_t st) {
+                                      const float2* tw, float alpha, int prec, cudaStream_t st) {
   const int kp = plane_g_kp(c);
   const int B = c->batch, H = c->hidden_dim, N = c->output_dim, dx = c->dim_x;
   switch (c->dim_y) {
-    case 64: return plane_g_invmix_run_64(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 128: return plane_g_invmix_run_128(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 256: return plane_g_invmix_run_256(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 512: return plane_g_invmix_run_512(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 1024: return plane_g_invmix_run_1024(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 64: return plane_g_invmix_run_64(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 128: return plane_g_invmix_run_128(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 256: return plane_g_invmix_run_256(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 512: return plane_g_invmix_run_512(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 1024: return plane_g_invmix_run_1024(kp, A, w, Cs, y, B, H, N, dx, tw, alpha, prec, st);
     default: return cudaErrorNotSupported;
   }
 }
@@ -715,11 +715,17 @@ static int plane_fusedmix_env() {  // TFNO_PLANE_FUSEDMIX=0/1 overrides the per-
 }
 
 bool plane2d_fusedmix(const tfno_cfg* c, int prec) {
-  if (prec != TFNO_FP32 || !plane2d_supported(c)) return false;
+  // FP32: SIMT mix warps; TF32 / 3xTF32: tcgen05 mix (BF16 keeps the standalone kind::f16 contraction)
+  if ((prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3) || !plane2d_supported(c)) return false;
   if ((int64_t)c->batch * ((c->output_dim + 7) / 8) > (1LL << 40)) return false;
   const int env = plane_fusedmix_env();
-  if (env == 0 || plane_g_invmix_smem(c) == 0) return false;
+  if (env == 0 || plane_g_invmix_smem(c, prec) == 0) return false;
   if (env == 1) return true;
+  // the tcgen05 mix inside the inverse is opt-in (TFNO_PLANE_FUSEDMIX=1): its A staging
+  // (global -> registers -> canonical K-major tiles, one K step per chunk) keeps too few
+  // loads in flight -- measured (profiles/r02/tcmix_ab.txt) C4 3xTF32 mix + inverse 8.08 ms
+  // vs 0.46 ms standalone tcgen05 CGEMM (W' image) + 5.91 ms inverse
+  if (prec != TFNO_FP32) return false;
   // default: where the standalone contraction is a large share of the layer and
   // every CTA has enough tasks to hide the first task's mix (the prologue) --
   // measured (profiles/r02/fusedmix_ab*.txt): C4 (H = N = 128, 13.8 tasks per
@@ -811,7 +817,7 @@ cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float
     cudaError_t e = (mix & 1) ? plane_g_run(c, -1, x, A, B * H, tw, 1.0f, st) : tuned_fwd(c, x, A, B * H, tw, true, st);
     if (e != cudaSuccess) return e;
     if (mark) mark(st);
-    if ((e = plane_g_invmix_run(c, A, w, Cm, y, tw, (float)(1.0 / ((double)c->dim_x * c->dim_y)), st)) !=
+    if ((e = plane_g_invmix_run(c, A, w, Cm, y, tw, (float)(1.0 / ((double)c->dim_x * c->dim_y)), prec, st)) !=
         cudaSuccess)
       return e;
     if (mark) mark(st);

@@ -97,54 +97,69 @@ cudaError_t g_inv(const float2* Cm, float2* y, int64_t planes, int dx, const flo
 
 // fused inverse + channel mix (plane_invmix_g): tasks of kMixGN output channels
 constexpr int kMixGN = 8;
-// A-ring depth: as many 16 KiB chunks (<= SA_MAX) as fit next to the inverse's buffers; >= 3
+// A-ring depth: as many 16 KiB chunks (<= SA_MAX) as fit next to the inverse's buffers; >= 3.
+// prec 1 / 3 (tensor-core mix): the ring holds the two staged A chunks (hi [, lo] canonical
+// tiles) and the W' tiles replace the packed W columns (depth >= 3 keeps three mbarriers).
 template <class G>
-int g_invmix_depth(int H, int dx, size_t* bytes) {
+int g_invmix_depth(int H, int dx, int prec, size_t* bytes) {
   using X = MixGeo<G::KXP * G::KYP>;
-  const size_t rest = sizeof(float4) * (size_t)H * kMixGN +
-                      sizeof(float2) * (2 * (size_t)G::KXP * G::KYP + (size_t)G::NTB * G::TB + G::DY + G::KXP + dx) +
-                      8 * (5 + 2 * X::SA_MAX);
+  const int npass = prec == 3 ? 2 : 1, Hp = (H + 3) & ~3;
+  const size_t wt = prec ? (size_t)npass * Hp * 128 : sizeof(float4) * (size_t)H * kMixGN;
+  const size_t rest = wt + sizeof(float2) * (2 * (size_t)G::KXP * G::KYP + (size_t)G::NTB * G::TB + G::DY + G::KXP + dx) +
+                      8 * (5 + 2 * X::SA_MAX) + 8;
   const size_t chunk = sizeof(float2) * (size_t)X::HC * X::MC, cap = 227 * 1024;
-  if (rest + 3 * chunk > cap) return 0;
-  int sa = (int)((cap - rest) / chunk);
+  const int need = prec ? (2 * npass * X::MC * 32 + (int)chunk - 1) / (int)chunk : 3;
+  const int lo = need > 3 ? need : 3;
+  if (rest + lo * chunk > cap) return 0;
+  int sa = prec ? lo : (int)((cap - rest) / chunk);
   if (sa > X::SA_MAX) sa = X::SA_MAX;
+  if (sa < lo) return 0;
   *bytes = rest + sa * chunk;
   return sa;
 }
 
 template <int DY, int KP>
-size_t g_invmix_bytes(int H, int dx, int* sa = nullptr) {
+size_t g_invmix_bytes(int H, int dx, int prec, int* sa = nullptr) {
   if constexpr (KP < 16 || KP > 64 || KP > DY) {
     return 0;
   } else {
     size_t b = 0;
-    const int d = g_invmix_depth<typename PGCfg<DY, KP>::GI>(H, dx, &b);
+    const int d = g_invmix_depth<typename PGCfg<DY, KP>::GI>(H, dx, prec, &b);
     if (sa) *sa = d;
     return d ? b : 0;
   }
 }
 
+template <int DY, int KP, int PREC>
+cudaError_t g_invmix_p(const float2* A, const float2* W, float2* Cs, float2* y, int B, int H, int N, int dx,
+                       const float2* tw, float alpha, cudaStream_t st) {
+  using G = typename PGCfg<DY, KP>::GI;
+  int sa = 0;
+  const size_t smem = g_invmix_bytes<DY, KP>(H, dx, PREC, &sa);
+  if (!smem) return cudaErrorNotSupported;
+  const int64_t tasks = (int64_t)B * ((N + kMixGN - 1) / kMixGN);
+  if (tasks <= 0) return cudaSuccess;
+  auto kern = plane_invmix_g<G, kMixGN, PREC>;
+  int grid = 0;
+  cudaError_t e = persistent_grid(kern, G::NTH + kMixThreads, smem, tasks, &grid);
+  if (e != cudaSuccess) return e;
+  if (grid > device_sms()) grid = device_sms();  // the C ring is sized for one CTA per SM
+  e = launch_pdl(kern, dim3(grid), dim3(G::NTH + kMixThreads), smem, st, A, W, Cs, y, B, H, N, dx, tw, alpha, sa);
+  if (e != cudaSuccess) return e;
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 template <int DY, int KP>
 cudaError_t g_invmix(const float2* A, const float2* W, float2* Cs, float2* y, int B, int H, int N, int dx,
-                     const float2* tw, float alpha, cudaStream_t st) {
+                     const float2* tw, float alpha, int prec, cudaStream_t st) {
   if constexpr (KP < 16 || KP > 64 || KP > DY) {
     return cudaErrorNotSupported;
   } else {
-    using G = typename PGCfg<DY, KP>::GI;
-    int sa = 0;
-    const size_t smem = g_invmix_bytes<DY, KP>(H, dx, &sa);
-    if (!smem) return cudaErrorNotSupported;
-    const int64_t tasks = (int64_t)B * ((N + kMixGN - 1) / kMixGN);
-    if (tasks <= 0) return cudaSuccess;
-    auto kern = plane_invmix_g<G, kMixGN>;
-    int grid = 0;
-    cudaError_t e = persistent_grid(kern, G::NTH + kMixThreads, smem, tasks, &grid);
-    if (e != cudaSuccess) return e;
-    if (grid > device_sms()) grid = device_sms();  // the C ring is sized for one CTA per SM
-    e = launch_pdl(kern, dim3(grid), dim3(G::NTH + kMixThreads), smem, st, A, W, Cs, y, B, H, N, dx, tw, alpha, sa);
-    if (e != cudaSuccess) return e;
-    ++g_launches;
-    return cudaGetLastError();
+    if (prec == 0) return g_invmix_p<DY, KP, 0>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
+    if (prec == 1) return g_invmix_p<DY, KP, 1>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
+    if (prec == 3) return g_invmix_p<DY, KP, 3>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
+    return cudaErrorNotSupported;
   }
 }
 
@@ -170,21 +185,21 @@ cudaError_t g_dispatch(int KP, int dir, const float2* in, float2* out, int64_t p
 }
 
 template <int DY>
-size_t g_invmix_query(int KP, int H, int dx) {
+size_t g_invmix_query(int KP, int H, int dx, int prec) {
   switch (KP) {
-    case 16: return g_invmix_bytes<DY, 16>(H, dx);
-    case 32: return g_invmix_bytes<DY, 32>(H, dx);
-    case 64: return g_invmix_bytes<DY, 64>(H, dx);
+    case 16: return g_invmix_bytes<DY, 16>(H, dx, prec);
+    case 32: return g_invmix_bytes<DY, 32>(H, dx, prec);
+    case 64: return g_invmix_bytes<DY, 64>(H, dx, prec);
     default: return 0;
   }
 }
 template <int DY>
 cudaError_t g_invmix_dispatch(int KP, const float2* A, const float2* W, float2* Cs, float2* y, int B, int H, int N,
-                              int dx, const float2* tw, float alpha, cudaStream_t st) {
+                              int dx, const float2* tw, float alpha, int prec, cudaStream_t st) {
   switch (KP) {
-    case 16: return g_invmix<DY, 16>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 32: return g_invmix<DY, 32>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
-    case 64: return g_invmix<DY, 64>(A, W, Cs, y, B, H, N, dx, tw, alpha, st);
+    case 16: return g_invmix<DY, 16>(A, W, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 32: return g_invmix<DY, 32>(A, W, Cs, y, B, H, N, dx, tw, alpha, prec, st);
+    case 64: return g_invmix<DY, 64>(A, W, Cs, y, B, H, N, dx, tw, alpha, prec, st);
     default: return cudaErrorNotSupported;
   }
 }
@@ -199,14 +214,15 @@ cudaError_t TFNO_CAT(plane_g_run_, PLANE_G_DY)(int KP, int dir, const float2* in
                                                cudaStream_t st) {
   return g_dispatch<PLANE_G_DY>(KP, dir, in, out, planes, dx, kx, ky, tw, scale, st);
 }
-// fused inverse + channel mix: shared-memory bytes (0 = unsupported) and launch
-size_t TFNO_CAT(plane_g_invmix_smem_, PLANE_G_DY)(int KP, int H, int dx) {
-  return g_invmix_query<PLANE_G_DY>(KP, H, dx);
+// fused inverse + channel mix (prec 0 FP32 SIMT, 1 TF32, 3 3xTF32 tcgen05): shared-memory
+// bytes (0 = unsupported) and launch
+size_t TFNO_CAT(plane_g_invmix_smem_, PLANE_G_DY)(int KP, int H, int dx, int prec) {
+  return g_invmix_query<PLANE_G_DY>(KP, H, dx, prec);
 }
 cudaError_t TFNO_CAT(plane_g_invmix_run_, PLANE_G_DY)(int KP, const float2* A, const float2* W, float2* Cs,
                                                       float2* y, int B, int H, int N, int dx, const float2* tw,
-                                                      float alpha, cudaStream_t st) {
-  return g_invmix_dispatch<PLANE_G_DY>(KP, A, W, Cs, y, B, H, N, dx, tw, alpha, st);
+                                                      float alpha, int prec, cudaStream_t st) {
+  return g_invmix_dispatch<PLANE_G_DY>(KP, A, W, Cs, y, B, H, N, dx, tw, alpha, prec, st);
 }
 
 }  // namespace tfno

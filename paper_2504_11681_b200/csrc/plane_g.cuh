@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "tcgen05.cuh"
 
 namespace tfno {
 
@@ -464,7 +465,22 @@ struct MixGeo {
   static_assert(MC % 128 == 0 && MQ % MC == 0, "mode chunking");
 };
 
-template <class G, int GN>
+// PREC 0: FP32 SIMT mix (above).  PREC 1 / 3: the mix on the tensor cores --
+// tcgen05.mma kind::tf32 (TF32, or 3xTF32 = hi*hi + hi*lo + lo*hi with
+// lo = x - tf32(x)), M = 128 modes (TMEM lanes) x N = 2*GN real columns
+// (re / im of the GN output channels) x K = 8 (4 hidden channels, real-
+// embedded: K' = 2h + c, W'[2h+c][2n+c'] = [[Wr, Wi], [-Wi, Wr]][c][c']).
+// The task's whole C (MQ/128 mode tiles x 2*GN columns, <= 512 columns) sits in
+// TMEM; the mix warps stage A (global -> registers -> K-major canonical
+// shared tiles, split hi/lo), one elected thread issues the MMAs and commits
+// to an mbarrier per stage, and at the end of the task the four mix warps
+// read their TMEM lane quarters (tcgen05.ld) into the C ring.
+template <int MQ>
+__host__ __device__ constexpr int invmix_tmem_cols() {
+  return (MQ / 128) * 16 <= 32 ? 32 : (MQ / 128) * 16 <= 64 ? 64 : (MQ / 128) * 16 <= 128 ? 128 : (MQ / 128) * 16 <= 256 ? 256 : 512;
+}
+
+template <class G, int GN, int PREC = 0>
 __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
     plane_invmix_g(const float2* __restrict__ Ain, const float2* __restrict__ W, float2* __restrict__ Cs,
                    float2* __restrict__ y, int B, int H, int N, int dx, const float2* __restrict__ twg,
@@ -475,9 +491,12 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
   using X = MixGeo<MQ>;
   constexpr int MC = X::MC, MI = X::MI, HC = X::HC;
   extern __shared__ __align__(128) uint8_t smem[];
-  float2* ring = reinterpret_cast<float2*>(smem);          // SA x HC x MC (TMA targets)
-  float4* Wt = reinterpret_cast<float4*>(ring + SA * HC * MC);  // H x GN packed W columns
-  float2* cin = reinterpret_cast<float2*>(Wt + (size_t)H * GN);  // MQ (TMA target)
+  constexpr int NPASS = PREC == 3 ? 2 : 1;
+  static_assert(PREC == 0 || GN == 8, "tensor-core mix: N = 16 real columns");
+  float2* ring = reinterpret_cast<float2*>(smem);          // SA x HC x MC (TMA targets / TC: A stages)
+  float4* Wt = reinterpret_cast<float4*>(ring + SA * HC * MC);  // H x GN packed W columns (TC: W' tiles)
+  const int Hp = (H + 3) & ~3;
+  float2* cin = reinterpret_cast<float2*>(Wt + (size_t)(PREC ? NPASS * Hp : H) * GN);  // MQ (TMA target)
   float2* Gb = cin + MQ;                                   // MQ
   float2* tb = Gb + MQ;                                    // NTB x TB
   float2* twy = tb + G::NTB * G::TB;
@@ -488,6 +507,7 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
   uint64_t* cfree = cready + 2;                            // [2] C slot read back (1 arrival)
   uint64_t* afull = cfree + 2;                             // [SA_MAX]
   uint64_t* aempty = afull + X::SA_MAX;                    // [SA_MAX] (4 warp arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + X::SA_MAX);  // TC: TMEM base address
 
   const int tid = threadIdx.x;
   const int R = dx / KXP;
@@ -515,6 +535,155 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
   pdl_wait();
   pdl_launch_dependents();
 
+  if (PREC != 0 && tid >= NTH) {
+    if constexpr (PREC != 0) {
+    // ================= mix warps, tcgen05 contraction
+    constexpr int NT = MC / 128;                // M tiles per chunk
+    constexpr int NMB = MQ / MC;
+    constexpr int A_LBO = 2048, B_LBO = 256;    // K-group strides (16 M / 2 N' groups of 128 B)
+    constexpr int ATILE = 128 * 8 * 4;          // one M tile x one K step (K' = 8), bytes
+    constexpr int STAGE = NPASS * NT * ATILE;
+    constexpr int NCOLS = invmix_tmem_cols<MQ>();
+    constexpr uint32_t IDESC = tc::make_idesc(128, 2 * GN, true);
+    constexpr int AI = NT;                      // (mode pair, channel pair) items per thread
+    const int ct = tid - NTH, mw = ct >> 5, lane = tid & 31;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(ring);
+    uint8_t* wp = reinterpret_cast<uint8_t*>(Wt);
+    const int wpass = Hp * 128;                 // bytes of one W' pass (K' = 2 Hp rows of 16 columns)
+    uint64_t* mmadone = afull;                  // [2] a stage's MMAs completed
+    uint64_t* tdone = afull + 2;                // the task's MMAs completed
+    if (mw == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::saddr(tslot)),
+                   "n"(NCOLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    named_bar(kMixBar, kMixThreads);
+    tc::fence_after();
+    const uint32_t tmem = *tslot;
+    const int NHC = Hp / 4;
+    const int64_t per_task = (int64_t)NMB * NHC;
+    const int64_t nch = nmine * per_task;
+    float4 ra[AI][2];
+    auto load_chunk = [&](int64_t c) {
+      const int64_t k = c / per_task;
+      const int r = (int)(c - k * per_task), mb = r / NHC, hc = r % NHC;
+      const int64_t b = (blockIdx.x + k * gridDim.x) / NG;
+#pragma unroll
+      for (int i = 0; i < AI; ++i) {
+        const int idx = ct + i * kMixThreads, mp = idx % (MC / 2), hp = idx / (MC / 2);
+        const int m = mb * MC + 2 * mp, h = hc * 4 + 2 * hp;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+          ra[i][rr] = (h + rr < H) ? __ldg(reinterpret_cast<const float4*>(Ain + ((b * H + h + rr) * (int64_t)MQ + m)))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto store_chunk = [&](int st) {
+      uint8_t* sA = stg + st * STAGE;
+#pragma unroll
+      for (int i = 0; i < AI; ++i) {
+        const int idx = ct + i * kMixThreads, mp = idx % (MC / 2), hp = idx / (MC / 2);
+        const int m = 2 * mp, t = m / 128, ml = m % 128;
+        const float4 v0 = ra[i][0], v1 = ra[i][1];  // (re, im) of modes m, m+1 at h; at h+1
+        const float4 r0 = make_float4(v0.x, v0.y, v1.x, v1.y), r1 = make_float4(v0.z, v0.w, v1.z, v1.w);
+        const uint32_t o0 = t * ATILE + cm_off(ml, 4 * hp, A_LBO), o1 = t * ATILE + cm_off(ml + 1, 4 * hp, A_LBO);
+        if constexpr (NPASS == 1) {
+          *reinterpret_cast<float4*>(sA + o0) = r0;
+          *reinterpret_cast<float4*>(sA + o1) = r1;
+        } else {
+          const float4 h0 = hi4(r0), h1 = hi4(r1);
+          *reinterpret_cast<float4*>(sA + o0) = h0;
+          *reinterpret_cast<float4*>(sA + o1) = h1;
+          *reinterpret_cast<float4*>(sA + NT * ATILE + o0) = sub4(r0, h0);
+          *reinterpret_cast<float4*>(sA + NT * ATILE + o1) = sub4(r1, h1);
+        }
+      }
+    };
+    int64_t gch = 0;
+    if (nch > 0) load_chunk(0);
+    for (int64_t k = 0; k < nmine; ++k) {
+      const int64_t t = blockIdx.x + k * gridDim.x;
+      const int n0 = (int)(t % NG) * GN;
+      const int gn = min(GN, N - n0);
+      named_bar(kMixBar, kMixThreads);  // the previous task's MMAs have completed (tdone): W' is free
+      // W' of the task, K-major canonical: row n' = 2n + c' holds K' = 2h + c
+      for (int i = ct; i < GN * (Hp / 2); i += kMixThreads) {
+        const int nl = i % GN, hp = i / GN, h = 2 * hp;
+        const bool okn = nl < gn;
+        const float2 w0 = (okn && h < H) ? __ldg(&W[(int64_t)h * N + n0 + nl]) : make_float2(0.f, 0.f);
+        const float2 w1 = (okn && h + 1 < H) ? __ldg(&W[(int64_t)(h + 1) * N + n0 + nl]) : make_float2(0.f, 0.f);
+        const float4 re_row = make_float4(w0.x, -w0.y, w1.x, -w1.y), im_row = make_float4(w0.y, w0.x, w1.y, w1.x);
+        const uint32_t o0 = cm_off(2 * nl, 4 * hp, B_LBO), o1 = cm_off(2 * nl + 1, 4 * hp, B_LBO);
+        if constexpr (NPASS == 1) {
+          *reinterpret_cast<float4*>(wp + o0) = re_row;
+          *reinterpret_cast<float4*>(wp + o1) = im_row;
+        } else {
+          const float4 h0 = hi4(re_row), h1 = hi4(im_row);
+          *reinterpret_cast<float4*>(wp + o0) = h0;
+          *reinterpret_cast<float4*>(wp + o1) = h1;
+          *reinterpret_cast<float4*>(wp + wpass + o0) = sub4(re_row, h0);
+          *reinterpret_cast<float4*>(wp + wpass + o1) = sub4(im_row, h1);
+        }
+      }
+      const int s = (int)(k & 1);
+      if (k >= 2) mbar_wait(&cfree[s], (uint32_t)(((k >> 1) - 1) & 1));  // the inverse has read slot s back
+      float2* cdst = myC + (int64_t)s * GN * MQ;
+#pragma unroll 1
+      for (int mb = 0; mb < NMB; ++mb) {
+#pragma unroll 1
+        for (int hc = 0; hc < NHC; ++hc, ++gch) {
+          const int st = (int)(gch & 1);
+          if (gch >= 2) mbar_wait(&mmadone[st], (uint32_t)(((gch - 2) >> 1) & 1));  // stage st drained
+          store_chunk(st);
+          if (gch + 1 < nch) load_chunk(gch + 1);
+          fence_proxy_async();  // generic smem stores -> the tensor core's reads
+          named_bar(kMixBar, kMixThreads);
+          if (ct == 0) {
+            tc::fence_after();
+            const uint32_t a0 = tc::saddr(stg + st * STAGE), b0 = tc::saddr(wp) + 2 * hc * B_LBO;
+#pragma unroll
+            for (int tt = 0; tt < NT; ++tt) {
+              const uint32_t d = tmem + (uint32_t)((mb * NT + tt) * 2 * GN);
+              const uint64_t ad = tc::make_desc(a0 + tt * ATILE, A_LBO, 128), bd = tc::make_desc(b0, B_LBO, 128);
+              tc::mma_tf32(d, ad, bd, IDESC, hc > 0 ? 1u : 0u);
+              if constexpr (NPASS == 2) {
+                tc::mma_tf32(d, ad, tc::make_desc(b0 + wpass, B_LBO, 128), IDESC, 1u);
+                tc::mma_tf32(d, tc::make_desc(a0 + NT * ATILE + tt * ATILE, A_LBO, 128), bd, IDESC, 1u);
+              }
+            }
+            tc::commit(&mmadone[st]);
+          }
+        }
+      }
+      if (ct == 0) tc::commit(tdone);
+      mbar_wait(tdone, (uint32_t)(k & 1));
+      tc::fence_after();
+      // drain: this warp's 32 TMEM lanes = modes tg*128 + 32*mw + lane of every mode tile tg
+#pragma unroll 1
+      for (int tp = 0; tp < MQ / 256; ++tp) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(mw * 32) << 16) + (uint32_t)(tp * 32), v);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int m = (2 * tp + hf) * 128 + mw * 32 + lane;
+#pragma unroll
+          for (int g = 0; g < GN; ++g)
+            if (g < gn)
+              cdst[(int64_t)g * MQ + m] = make_float2(alpha * v[hf * 16 + 2 * g], alpha * v[hf * 16 + 2 * g + 1]);
+        }
+      }
+      tc::fence_before();   // TMEM reads complete before the next task's MMAs (after the next barrier)
+      fence_proxy_async_global();  // the C tile is read back with cp.async.bulk
+      mbar_arrive(&cready[s]);
+    }
+    tc::fence_before();
+    named_bar(kMixBar, kMixThreads);
+    if (mw == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(NCOLS) : "memory");
+    }
+    return;
+  }
   if (tid >= NTH) {
     // ================= mix warps
     const int ct = tid - NTH;

@@ -131,36 +131,39 @@ print("ok")
 _FUSEDMIX_CODE = r"""
 import numpy as np, paper_2504_11681_b200 as T
 from oracle import fnofuse_port as O
-FM = "@FM@"
+FM, PREC, TOL = "@FM@", "@PREC@", @TOL@
 want = "plane-fft2d|plane-mix-ifft2d" if FM == "1" else "plane-fft2d|cgemm-modes|plane-ifft2d"
 for s in [(2, 3, 13, 512, 512, 64, 64), (64, 8, 64, 64, 64, 16, 16), (40, 21, 19, 128, 128, 32, 32),
           (3, 70, 9, 256, 128, 20, 12), (2, 5, 8, 64, 512, 16, 16), (1, 300, 17, 128, 64, 16, 16),
           (2, 2, 3, 256, 256, 16, 16), (600, 2, 5, 64, 64, 8, 8)]:
     cfg = T.FnoLayerConfig(*s, rank=2)
-    d = T.layer_schedule(cfg, "fully_fused")[1]
+    d = T.layer_schedule(cfg, "fully_fused", PREC)[1]
     kp = max(8, 1 << (max(s[5], s[6]) - 1).bit_length())
     assert d == want or kp not in (16, 32, 64), (s, d)
     x, w = O.random_inputs(cfg, 7 + s[0])
-    out, _ = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused", precision=PREC)
     err = T.max_rel_error(out.data, O.reference_layer(cfg, x, w))
-    assert err < 1e-5, (s, err)
-    b, _ = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
+    assert err < TOL, (s, err)
+    b, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused", precision=PREC)
     assert np.array_equal(out.data, b.data), s
 print("ok")
 """
 
 
-@pytest.mark.parametrize("fusedmix", ["0", "1"])
-def test_fused_mix_inverse(fusedmix):
+@pytest.mark.parametrize("fusedmix,prec,tol", [("0", "fp32", 1e-5), ("1", "fp32", 1e-5), ("1", "tf32x3", 1e-5),
+                                               ("1", "tf32", 1e-3), ("0", "tf32x3", 1e-5)])
+def test_fused_mix_inverse(fusedmix, prec, tol):
     """plane_invmix_g (channel mix inside the inverse kernel, C in a per-CTA
     two-task ring) and the standalone-CGEMM schedule: ragged N (tasks of 8
     output channels), H not a multiple of the A chunk, more tasks than CTAs
     (the C ring and the A ring wrap many times), every fused KP (16/32/64),
     non-square planes, the C4 plane shape; FP32 bar vs the float64
-    composition, bitwise determinism."""
+    composition, bitwise determinism.  prec tf32 / tf32x3: the tcgen05 mix
+    (TMEM accumulators, K-major canonical A / W' tiles), bars 1e-3 / 1e-5."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, TFNO_PLANE_FUSEDMIX=fusedmix, PYTHONPATH=root)
-    r = subprocess.run([sys.executable, "-c", _FUSEDMIX_CODE.replace("@FM@", fusedmix)], env=env,
+    code = _FUSEDMIX_CODE.replace("@FM@", fusedmix).replace("@PREC@", prec).replace("@TOL@", repr(tol))
+    r = subprocess.run([sys.executable, "-c", code], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 

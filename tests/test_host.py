@@ -112,8 +112,10 @@ def test_schedules_and_workspace():
     # tiles in a per-CTA two-task ring (SMs x 2 x 8 planes; 148 SMs without a device)
     assert T.layer_schedule(c4, "fully_fused") == (2, "plane-fft2d|plane-mix-ifft2d")
     assert T.workspace_bytes(c4, "fully_fused") == (128 * 128 + 148 * 2 * 8) * 64 * 64 * 8
-    # tensor-core contractions keep the standalone tcgen05 CGEMM between the plane kernels
-    assert T.layer_schedule(c4, "fully_fused", "tf32x3")[1] == "plane-fft2d|cgemm-modes|plane-ifft2d"
+    # tensor-core precisions keep the standalone tcgen05 CGEMM (W' image) between the plane kernels
+    # (the tcgen05 mix inside the inverse is opt-in: TFNO_PLANE_FUSEDMIX=1)
+    for p in ("tf32x3", "tf32", "bf16"):
+        assert T.layer_schedule(c4, "fully_fused", p)[1] == "plane-fft2d|cgemm-modes|plane-ifft2d"
     c1 = T.FnoLayerConfig(16, 64, 64, 1, 128, 1, 32, 1)
     assert T.layer_schedule(c1, "fully_fused") == (1, "fused1d-fft-cgemm-ifft")  # one launch (fused1d.cu)
     assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused-fft-cgemm|y-ifft")

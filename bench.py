@@ -157,6 +157,24 @@ def load_traffic(workload, kernel):
         return None
 
 
+def load_n3(workload):
+    """N3 evidence: ncu launch counts and DRAM bytes of our fully_fused layer and of the
+    staged cuFFT+cuBLAS pipeline, captured in one process (tools/n3_traffic.py; the newest
+    profiles/rNN/n3_traffic.json).  A committed capture, labelled as such."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "n3_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f).get(workload)
+    except Exception:
+        return None
+    if d:
+        d = dict(d, source=os.path.relpath(files[-1], ROOT) + " (ncu, committed capture, not this run)")
+    return d
+
+
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # pip --target install of the unmodified reference
 
 
@@ -529,6 +547,9 @@ def run_ours(args):
         best = min((v["ms"] for v in base.values() if isinstance(v, dict) and "ms" in v), default=None)
         if best:
             base["speedup_vs_best_unfused"] = round(best / ms, 3)
+        n3 = load_n3(args.workload if args.workload != "C5" else "C5L")
+        if n3:
+            base["ncu_launch_and_dram_reduction"] = n3
         result["baselines"] = base
         del y2
         torch.cuda.empty_cache()

@@ -150,6 +150,10 @@ int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* 
                     int64_t a_bs, const void* W, int64_t w_ks, int64_t w_ns, int64_t w_bs, void* C, int64_t c_ms,
                     int64_t c_ns, int64_t c_bs, float alpha, int prec, void* stream);
 
+/* out[i] = sum_{b < batch} in[b*n + i] (complex64, ascending b: deterministic); the batch
+ * reduction of the per-element grad_W partials of the backward pass (extension). */
+int tfno_batch_sum(const void* in, int64_t batch, int64_t n, void* out, void* stream);
+
 /* Plane modulation (symmetric +-mode truncation, an extension beyond the reference):
  * out[p][x][y] = scale * in[p][x][y] * exp(sign * 2*pi*i * (sx*x/dx + sy*y/dy)), sign = +1 / -1.
  * Modulating by (+keep_x/2, +keep_y/2) before and (-keep_x/2, -keep_y/2) after the first-keep

@@ -57,7 +57,9 @@ def layer_backward(cfg: FnoLayerConfig, x, w, grad_y, need_x: bool = True, need_
                               part.data_ptr(), N, 1, H * N, 1.0 / (cfg.dim_x * cfg.dim_y),
                               _device.stream_ptr(None))
         check(rc, "tfno_cgemm")
-        grad_w = part.sum(dim=0)
+        grad_w = t.empty((H, N), dtype=t.complex64, device=x.device)
+        check(lib().tfno_batch_sum(part.data_ptr(), B, H * N, grad_w.data_ptr(), _device.stream_ptr(None)),
+              "tfno_batch_sum")
     return grad_x, grad_w
 
 

@@ -568,6 +568,13 @@ int tfno_cgemm(int64_t M, int64_t N, int64_t K, int64_t batch, const void* A, in
   return cuda_status(launch_cgemm(g, (cudaStream_t)stream));
 }
 
+int tfno_batch_sum(const void* in, int64_t batch, int64_t n, void* out, void* stream) {
+  if (batch < 0 || n < 0) return TFNO_EINVAL;
+  if (n == 0) return TFNO_OK;
+  if (!in || !out) return TFNO_EINVAL;
+  return cuda_status(launch_batch_sum((const float2*)in, batch, n, (float2*)out, (cudaStream_t)stream));
+}
+
 int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, const void* in, void* out, float scale,
                   void* stream) {
   if (planes < 0 || !pow2(dx) || !pow2(dy) || dx > TFNO_TW_MAX || dy > TFNO_TW_MAX || (sign != 1 && sign != -1))

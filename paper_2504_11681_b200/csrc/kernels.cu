@@ -744,6 +744,25 @@ cudaError_t launch_modulate(const float2* in, float2* out, int64_t planes, int d
   return cudaGetLastError();
 }
 
+// out[i] = sum over b (ascending, fixed order: deterministic) of in[b][i] -- the batch
+// reduction of per-batch-element partial products (grad_W of the backward pass)
+__global__ void batch_sum_kernel(const float2* __restrict__ in, int64_t batch, int64_t n, float2* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float2 s = make_float2(0.f, 0.f);
+    for (int64_t b = 0; b < batch; ++b) s = cadd(s, __ldg(&in[b * n + i]));
+    out[i] = s;
+  }
+}
+
+cudaError_t launch_batch_sum(const float2* in, int64_t batch, int64_t n, float2* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  batch_sum_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, batch, n, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // staged baseline copy passes: dst[plane][x][y] = x<cx && y<cy ? scale*src : 0
 // ------------------------------------------------------------------------
 __global__ void pad_truncate_kernel(const float2* __restrict__ src, int64_t planes, int sx, int sy,

@@ -79,6 +79,7 @@ inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s
   return cudaErrorNotSupported;
 }
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
+cudaError_t launch_batch_sum(const float2* in, int64_t batch, int64_t n, float2* out, cudaStream_t s);
 cudaError_t launch_modulate(const float2* in, float2* out, int64_t planes, int dx, int dy, int sx, int sy, int sign,
                             float scale, const float2* tw, cudaStream_t s);
 // warp-synchronous register FFT rows (warpfft.cu): n in {256, 1024}, keep / src_len <= n/4

@@ -11,4 +11,4 @@ timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram_
   --clock-control none --csv --log-file gpurun_out/n3_raw.csv python tools/n3_traffic.py run C3 C4 C5L C1 C2-N1024-H64-B1024 > gpurun_out/n3_run.log 2>&1
 python tools/n3_traffic.py summarize gpurun_out/n3_raw.csv > gpurun_out/n3_traffic.json 2>gpurun_out/n3_sum.err
 tail -2 gpurun_out/n3_run.log; head -c 300 gpurun_out/n3_traffic.json
-bash tools/r2_sweep.sh r2b
+bash tools/r02/r2_sweep.sh r2b

@@ -1,4 +1,4 @@
-# round-1 HostPipeline (per-stream H2D -> layer -> D2H), kept only for the e2e A/B in tools/r2_e2e.sh
+# round-1 HostPipeline (per-stream H2D -> layer -> D2H), kept only for the e2e A/B in tools/r02/r2_e2e.sh
 import ctypes
 from paper_2504_11681_b200 import _device
 from paper_2504_11681_b200.core import FnoLayerConfig

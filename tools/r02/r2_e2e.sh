@@ -11,7 +11,7 @@ xh = torch.empty(x.shape, dtype=torch.complex64, pin_memory=True); xh.copy_(x); 
 yh = torch.empty(xh.shape, dtype=torch.complex64, pin_memory=True)
 w = torch.view_as_complex(torch.randn((128, 128, 2)))
 torch.cuda.empty_cache()
-import sys; sys.path.insert(0, "tools/ab"); import old_hostpipeline as OLD
+import sys; sys.path.insert(0, "tools/r02/ab"); import old_hostpipeline as OLD
 for chunk, nbuf, ncopy in [("old", 4, 3), (1, 4, 2), ("old", 2, 3), (4, 4, 2), ("old", 4, 4), (2, 4, 2), ("old", 1, 3)]:
     pipe = (OLD.HostPipeline(cfg, chunk=nbuf, nstreams=ncopy) if chunk == "old" else
             T.pipeline.HostPipeline(cfg, chunk=chunk, nbuf=nbuf, ncopy=ncopy))

@@ -134,6 +134,7 @@ def stage_algorithmic_bytes(cfg, desc):
         "y-fft": B * H * kx * dy + B * H * kx * ky,
         "fused-fft-cgemm-ifft": B * H * kx * dy + B * N * kx * dy + H * N,
         "fused1d-fft-cgemm-ifft": B * H * kx * dy + B * N * kx * dy + H * N,
+        "tiny1d-fft-cgemm-ifft": B * H * kx * dy + B * N * kx * dy + H * N,
         "fused-fft-cgemm": B * H * kx * dy + B * N * kx * ky + H * N,
         "fused-cgemm-ifft": B * H * kx * ky + B * N * kx * dy + H * N,
         "cgemm": B * H * kx * ky + B * N * kx * ky + H * N,

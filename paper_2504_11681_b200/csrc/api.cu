@@ -151,6 +151,7 @@ cudaError_t launch_pencils_auto(const FftPencilArgs& a, int dir, cudaStream_t st
 struct Sched {
   bool staged = false, plane2d = false, rows_fast = false, warp_fused = false, f1 = false;
   bool plane_mix = false;  // rank-2 plane path with the channel mix fused into the inverse
+  bool tiny = false;       // small latency-bound 1D layer: tiny1d kernel
   int rows_NT = 0, f1_split = 1, f1_cluster = 1;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
@@ -183,6 +184,24 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
       s.desc = "plane-fft2d|cgemm-modes|plane-ifft2d";
     }
     return s;
+  }
+  {
+    // latency-bound small 1D layers (C1): one independent CTA per (batch element, 8 output
+    // channels), forward FFTs recomputed per CTA; only while the CTAs fit one wave
+    static int tiny_env = -2;
+    if (tiny_env == -2) {
+      const char* e = getenv("TFNO_TINY1D");
+      tiny_env = e ? atoi(e) : -1;
+    }
+    const int64_t ctas = g.B * ((g.N + 7) / 8);
+    if (g.rank == 1 && mode == TFNO_FULLY_FUSED && prec == TFNO_FP32 && tiny_env != 0 &&
+        tiny1d_supported((int)g.dy, (int)g.ky, (int)g.B, (int)g.H, (int)g.N) &&
+        (tiny_env == 1 || ctas <= num_sms_api())) {
+      s.tiny = true;
+      s.launches = 1;
+      s.desc = "tiny1d-fft-cgemm-ifft";
+      return s;
+    }
   }
   FusedArgs fa{};
   int NT = 0;
@@ -407,7 +426,9 @@ int staged_forward(const tfno_cfg* c, const float2* x, const float2* w, float2* 
 }
 
 // the channel mix runs as a standalone CGEMM (plane2d path or the unfused row schedule)
-bool sched_has_cgemm(const Sched& s) { return (s.plane2d && !s.plane_mix) || (!s.plane2d && !s.staged && !s.fg && !s.gi); }
+bool sched_has_cgemm(const Sched& s) {
+  return (s.plane2d && !s.plane_mix) || (!s.plane2d && !s.tiny && !s.staged && !s.fg && !s.gi);
+}
 
 size_t wimg_bytes_for(const tfno_cfg* c, int mode, int prec) {
   Sched s = make_sched(c, mode, prec);
@@ -745,6 +766,11 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
   stage_begin(st);
   if (s.plane2d)
     return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, wimg_ready, st, &stage_mark));
+  if (s.tiny) {
+    const cudaError_t te = launch_tiny1d(x, w, y, (int)g.B, (int)g.H, (int)g.N, (int)g.ky, tw, st);
+    if (te == cudaSuccess) stage_mark(st);
+    return cuda_status(te);
+  }
 
   cudaError_t e;
   const float2* src = x;

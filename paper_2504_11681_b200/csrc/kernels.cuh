@@ -123,6 +123,26 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled(2) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}  // SM count of the current device (cached per device)
+}
+// the same with PDL at level 1 (on by default): the 1D layer kernels
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl1(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(1) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+// small latency-bound 1D layers (N = 128, keep <= 64): one kernel, CTA = (batch element, 8 output channels)
+bool tiny1d_supported(int n, int keep, int B, int H, int N);
+cudaError_t launch_tiny1d(const float2* x, const float2* W, float2* y, int B, int H, int N, int keep,
+                          const float2* tw, cudaStream_t s);  // SM count of the current device (cached per device)
 
 }  // namespace tfno

@@ -52,7 +52,8 @@ def _schedule(T, cfg):
 @pytest.mark.parametrize("case", CASES)
 def test_fused1d_vs_oracle(T, O, case):
     cfg = T.FnoLayerConfig(*case)
-    assert "fused1d" in _schedule(T, cfg), _schedule(T, cfg)
+    # C1-sized layers (one wave of (batch, 8-channel) CTAs) take the tiny1d kernel instead
+    assert "fused1d" in _schedule(T, cfg) or "tiny1d" in _schedule(T, cfg), _schedule(T, cfg)
     x, w = O.random_inputs(cfg, 2000 + sum(case))
     out, led = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
     ref = O.run_layer_values(cfg, x, w)
@@ -80,3 +81,49 @@ def test_fused1d_many_items_vs_unfused(T, n, h, keep):
     assert T.max_rel_error(a, b) < FP32_TOL
     assert torch.equal(y1, y3)
     assert np.isfinite(a).all()
+
+
+TINY = [
+    (16, 64, 64, 1, 128, 1, 32, 1),   # C1 exactly
+    (3, 64, 64, 1, 128, 1, 32, 1),
+    (5, 37, 21, 1, 128, 1, 20, 1),    # ragged H, N (last CTA has 5 channels), ragged keep
+    (2, 128, 8, 1, 128, 1, 64, 1),    # keep 64 (4 bin groups), H = 128
+    (4, 16, 30, 1, 128, 1, 1, 1),     # keep 1
+    (1, 200, 3, 1, 128, 1, 33, 1),    # H not a multiple of the 64-row batches of the teams
+]
+
+
+@pytest.mark.parametrize("case", TINY)
+def test_tiny1d_vs_oracle(T, O, case):
+    """tiny1d_kernel (one independent CTA per (batch element, 8 output
+    channels), forward FFTs recomputed per CTA) vs the oracle; bitwise
+    determinism; the fused1d kernel on the same inputs (TFNO_TINY1D off)
+    within the FP32 bar."""
+    cfg = T.FnoLayerConfig(*case)
+    assert _schedule(T, cfg) == "tiny1d-fft-cgemm-ifft", _schedule(T, cfg)
+    x, w = O.random_inputs(cfg, 3000 + sum(case))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+    err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w))
+    assert err < FP32_TOL, (case, err)
+    again, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+    assert np.array_equal(out.data, again.data)
+
+
+def test_tiny1d_off_keeps_fused1d():
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import paper_2504_11681_b200 as T
+from oracle import fnofuse_port as O
+cfg = T.FnoLayerConfig(16, 64, 64, 1, 128, 1, 32, 1)
+assert T.layer_schedule(cfg, "fully_fused")[1] == "fused1d-fft-cgemm-ifft"
+x, w = O.random_inputs(cfg, 1)
+out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+assert T.max_rel_error(out.data, O.run_layer_values(cfg, x, w)) < 1e-5
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=root, TFNO_TINY1D="0"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -193,10 +193,14 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
       const char* e = getenv("TFNO_TINY1D");
       tiny_env = e ? atoi(e) : -1;
     }
-    const int64_t ctas = g.B * ((g.N + 7) / 8);
-    if (g.rank == 1 && mode == TFNO_FULLY_FUSED && prec == TFNO_FP32 && tiny_env != 0 &&
-        tiny1d_supported((int)g.dy, (int)g.ky, (int)g.B, (int)g.H, (int)g.N) &&
-        (tiny_env == 1 || ctas <= num_sms_api())) {
+    // default where measured faster than the persistent fused kernel (profiles/r02/tiny2_ab.txt):
+    // N <= 256 rows, H <= 64, at most 32 output channels per CTA (C1 12.7 -> 6.9 us, N256-H64-B64
+    // 15.2 -> 13.0 us; N256-H128-B64 and N1024-H64-B64 are slower: 22.7 -> 30.6, 31.8 -> 42.1 us);
+    // TFNO_TINY1D=1 wherever the kernel fits, 0 never
+    const bool tiny_ok = tiny1d_supported((int)g.dy, (int)g.ky, (int)g.B, (int)g.H, (int)g.N);
+    const bool tiny_win = g.dy <= 256 && g.H <= 64 && tiny1d_channels_per_cta((int)g.B, (int)g.N) <= 32;
+    if (g.rank == 1 && mode == TFNO_FULLY_FUSED && prec == TFNO_FP32 && tiny_env != 0 && tiny_ok &&
+        (tiny_env == 1 || tiny_win)) {
       s.tiny = true;
       s.launches = 1;
       s.desc = "tiny1d-fft-cgemm-ifft";
@@ -767,7 +771,7 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
   if (s.plane2d)
     return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, wimg_ready, st, &stage_mark));
   if (s.tiny) {
-    const cudaError_t te = launch_tiny1d(x, w, y, (int)g.B, (int)g.H, (int)g.N, (int)g.ky, tw, st);
+    const cudaError_t te = launch_tiny1d(x, w, y, (int)g.dy, (int)g.B, (int)g.H, (int)g.N, (int)g.ky, tw, st);
     if (te == cudaSuccess) stage_mark(st);
     return cuda_status(te);
   }

@@ -140,9 +140,11 @@ inline cudaError_t launch_pdl1(void (*kern)(KArgs...), dim3 grid, dim3 block, si
   cfg.numAttrs = pdl_enabled(1) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
-// small latency-bound 1D layers (N = 128, keep <= 64): one kernel, CTA = (batch element, 8 output channels)
+// small latency-bound 1D layers (N = 128 / 256 / 1024): one kernel, CTA = (batch element, 8 / 32 / 64
+// output channels) with the grid within one wave of SMs
 bool tiny1d_supported(int n, int keep, int B, int H, int N);
-cudaError_t launch_tiny1d(const float2* x, const float2* W, float2* y, int B, int H, int N, int keep,
+int tiny1d_channels_per_cta(int B, int N);  // 8 / 32 / 64 (0: no one-wave grid)
+cudaError_t launch_tiny1d(const float2* x, const float2* W, float2* y, int n, int B, int H, int N, int keep,
                           const float2* tw, cudaStream_t s);  // SM count of the current device (cached per device)
 
 }  // namespace tfno

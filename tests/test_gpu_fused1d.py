@@ -90,17 +90,56 @@ TINY = [
     (2, 128, 8, 1, 128, 1, 64, 1),    # keep 64 (4 bin groups), H = 128
     (4, 16, 30, 1, 128, 1, 1, 1),     # keep 1
     (1, 200, 3, 1, 128, 1, 33, 1),    # H not a multiple of the 64-row batches of the teams
+    (64, 64, 64, 1, 256, 1, 32, 1),   # C2 N256-H64-B64 (32 channels per CTA)
+    (64, 128, 128, 1, 256, 1, 32, 1), # C2 N256-H128-B64 (64 channels per CTA)
+    (64, 64, 64, 1, 1024, 1, 128, 1), # C2 N1024-H64-B64 (32-lane teams)
+    (7, 50, 70, 1, 256, 1, 20, 1),    # ragged N / keep, 8 channels per CTA
+    (40, 33, 100, 1, 1024, 1, 100, 1),  # keep 100 -> 4 bin groups, 64 channels per CTA, ragged tail
+    (5, 20, 40, 1, 256, 1, 64, 1),    # keep 64 at N = 256
 ]
+
+
+def test_tiny1d_default_selection(T):
+    """tiny1d is the default only where it was measured faster (N <= 256, H <= 64, <= 32 channels per CTA)."""
+    for case, want in [((16, 64, 64, 1, 128, 1, 32, 1), "tiny1d"), ((64, 64, 64, 1, 256, 1, 32, 1), "tiny1d"),
+                       ((64, 128, 128, 1, 256, 1, 32, 1), "fused1d"), ((64, 64, 64, 1, 1024, 1, 128, 1), "fused1d")]:
+        assert _schedule(T, T.FnoLayerConfig(*case)).startswith(want), case
+
+
+_TINY_CODE = r"""
+import numpy as np, paper_2504_11681_b200 as T
+from oracle import fnofuse_port as O
+for case in CASES:
+    cfg = T.FnoLayerConfig(*case)
+    assert T.layer_schedule(cfg, "fully_fused")[1] == "tiny1d-fft-cgemm-ifft", case
+    x, w = O.random_inputs(cfg, 3000 + sum(case))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+    err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w))
+    assert err < 1e-5, (case, err)
+    again, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
+    assert np.array_equal(out.data, again.data), case
+print("ok")
+"""
+
+
+def test_tiny1d_forced_every_shape():
+    """TFNO_TINY1D=1: the kernel on every shape it fits (N = 128 / 256 / 1024, 8 / 32 / 64 channels
+    per CTA, ragged N and keep, 1..4 bin groups) vs the oracle, bitwise determinism."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _TINY_CODE.replace("CASES", repr(TINY))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=root, TFNO_TINY1D="1"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("case", TINY)
 def test_tiny1d_vs_oracle(T, O, case):
-    """tiny1d_kernel (one independent CTA per (batch element, 8 output
-    channels), forward FFTs recomputed per CTA) vs the oracle; bitwise
-    determinism; the fused1d kernel on the same inputs (TFNO_TINY1D off)
-    within the FP32 bar."""
+    """The default schedule (tiny1d where it wins, else fused1d) on the tiny
+    shapes vs the oracle; bitwise determinism."""
     cfg = T.FnoLayerConfig(*case)
-    assert _schedule(T, cfg) == "tiny1d-fft-cgemm-ifft", _schedule(T, cfg)
     x, w = O.random_inputs(cfg, 3000 + sum(case))
     out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fully_fused")
     err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w))

@@ -118,7 +118,7 @@ def test_schedules_and_workspace():
         assert T.layer_schedule(c4, "fully_fused", p)[1] == "plane-fft2d|cgemm-modes|plane-ifft2d"
     c1 = T.FnoLayerConfig(16, 64, 64, 1, 128, 1, 32, 1)
     assert T.layer_schedule(c1, "fully_fused") == (1, "tiny1d-fft-cgemm-ifft")  # one launch (tiny1d.cu)
-    assert T.layer_schedule(T.FnoLayerConfig(64, 64, 64, 1, 128, 1, 32, 1), "fully_fused") == \
+    assert T.layer_schedule(T.FnoLayerConfig(256, 64, 64, 1, 128, 1, 32, 1), "fully_fused") == \
         (1, "fused1d-fft-cgemm-ifft")  # more CTAs than one wave: the persistent fused kernel
     assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused-fft-cgemm|y-ifft")
     c2 = T.FnoLayerConfig(1024, 256, 256, 1, 256, 1, 32, 1)

@@ -68,3 +68,9 @@ cfg = T.FnoLayerConfig(1, 4, 4, 256, 256, 32, 32, 2)
 MG.spectrum_inverse(cfg, MG.spectrum_forward(cfg, rnd(1, 4, 256, 256)), (1, 4))
 torch.cuda.synchronize()
 print("ok spectrum")
+for shape in ((16, 64, 64, 1, 128, 1, 32, 1), (64, 64, 64, 1, 256, 1, 32, 1), (3, 20, 70, 1, 1024, 1, 100, 1)):
+    cfg = T.FnoLayerConfig(*shape)  # tiny1d (the last one only with TFNO_TINY1D=1; default fused1d otherwise)
+    x, w = rnd(cfg.batch, cfg.hidden_dim, cfg.dim_x, cfg.dim_y), rnd(cfg.hidden_dim, cfg.output_dim)
+    T.run_layer_device(cfg, x, w)
+    torch.cuda.synchronize()
+    print("ok tiny1d", shape, flush=True)

@@ -152,7 +152,7 @@ struct Sched {
   bool staged = false, plane2d = false, rows_fast = false, warp_fused = false, f1 = false;
   bool plane_mix = false;  // rank-2 plane path with the channel mix fused into the inverse
   bool tiny = false;       // small latency-bound 1D layer: tiny1d kernel
-  int rows_NT = 0, f1_split = 1, f1_cluster = 1;
+  int rows_NT = 0, f1_split = 1, f1_cluster = 1, f1_part = 0;
   bool fg = false, gi = false;  // which row fusions actually run
   bool need_A = false, need_C = false, need_s1 = false, need_mid = false;
   int launches = 0;
@@ -220,6 +220,24 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
   const bool tc_heavy = prec != TFNO_FP32 && g.H * g.N >= 128 * 128;
   const bool f1_full = fused1d_supported((int)g.dy, (int)g.ky, (int)g.H, (int)g.N);
   const int f1_forced = f1_full ? 0 : fused1d_split((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx);
+  // the partial fusions (K4 fused_fft_gemm / K5 fused_gemm_ifft) on the same kernel: its FFT + GEMM
+  // half writing C, or its GEMM + iFFT half reading the y-FFT's A (even keep: 16-byte bulk rows)
+  const bool part_mode = mode == TFNO_FUSED_FFT_GEMM || mode == TFNO_FUSED_GEMM_IFFT;
+  if (allow_f1 && part_mode && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1) && g.ky % 2 == 0) {
+    s.f1 = true;
+    s.f1_part = mode == TFNO_FUSED_FFT_GEMM ? 1 : 2;
+    s.f1_cluster = 1;
+    s.f1_split = f1_full ? 1 : f1_forced;
+    s.fg = s.f1_part == 1;
+    s.gi = s.f1_part == 2;
+    s.need_s1 = s.need_mid = (g.rank == 2);
+    s.need_A = !s.fg;
+    s.need_C = !s.gi;
+    const char* mid = s.fg ? "fused1d-fft-cgemm|y-ifft" : "y-fft|fused1d-cgemm-ifft";
+    s.desc = g.rank == 2 ? std::string("x-fft|") + mid + "|x-ifft" : std::string(mid);
+    s.launches = g.rank == 2 ? 4 : 2;
+    return s;
+  }
   if (allow_f1 && mode == TFNO_FULLY_FUSED && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1)) {
     s.f1 = true;
     s.f1_cluster = f1_full ? fused1d_cluster((int)g.dy, (int)g.ky, (int)g.H, (int)g.N, g.B * g.kx) : 1;
@@ -805,6 +823,7 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
       fa.NT = (s.warp_fused || s.f1) ? (int)g.N : s.rows_NT;
       fa.nsplit = s.f1 ? s.f1_split : 1;
       fa.cluster = s.f1 ? s.f1_cluster : 1;
+      fa.part = s.f1 ? s.f1_part : 0;
       fa.KC = rows_chunk((int)g.dy);
       fa.EC = fa.KC;
     } else {

@@ -145,7 +145,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 // reads of a half warp are both conflict free.
 __device__ __forceinline__ int tsw8(int r, int c) { return r * 16 + (c ^ (2 * r)); }
 
-template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS>
+// PART: 0 = the full layer; 1 = K4 (fused_fft_gemm: FFT + GEMM, the C tile goes to
+// a.C and the padded y-iFFT runs as its own pass); 2 = K5 (fused_gemm_ifft: the
+// kept bins are read from a.A -- written by the y-FFT pass -- instead of being
+// transformed, then GEMM + padded iFFT as usual)
+template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS, int PART = 0>
 __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
   // CS > 1: a cluster of CS CTAs shares each item: CTA r transforms and mixes
   // the hidden channels [r*H/CS, (r+1)*H/CS), the CS partial C tiles are summed
@@ -223,7 +227,10 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         const int64_t item = first + it * units;
         const int64_t g = item / S, n0 = (item % S) * NOUT;
         const int64_t bb = g / a.gx, pp = g % a.gx;
-        const float2* xg = a.x + bb * a.x_sb + pp * a.x_sp;
+        // PART 2 streams the y-FFT's kept bins (keep complex per row) instead of the input rows
+        const float2* xg = PART == 2 ? a.A + bb * a.a_sb + pp * a.a_sp : a.x + bb * a.x_sb + pp * a.x_sp;
+        const int64_t rstride = PART == 2 ? a.a_sh : a.x_sh;
+        const uint32_t rbytes = (uint32_t)((PART == 2 ? keep : N) * sizeof(float2));
         for (int c = 0; c < nchunks; ++c, ++kk) {
           const int rs = (int)(kk % NS);
           const int64_t use = kk / NS;
@@ -231,9 +238,8 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
           for (int t = 0; t < TEAMS; ++t) {
             const int b = t * NS + rs;
             if (use >= 1) mbar_wait(&empty[b], (uint32_t)((use - 1) & 1));
-            mbar_expect_tx(&full[b], N * sizeof(float2));
-            tma_load_1d(slots + b * N, xg + (int64_t)(h_off + c * KC + t) * a.x_sh, N * sizeof(float2), &full[b],
-                        pol_x);
+            mbar_expect_tx(&full[b], rbytes);
+            tma_load_1d(slots + b * N, xg + (int64_t)(h_off + c * KC + t) * rstride, rbytes, &full[b], pol_x);
           }
           const int ws = (int)(kk & 1);
           if (kk >= 2) mbar_wait(&wempty[ws], (uint32_t)(((kk >> 1) - 1) & 1));
@@ -346,7 +352,25 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
         mbar_wait(&full[b], (uint32_t)((kk / NS) & 1));
         const float2* slot = slots + b * N;
         const int s = (int)(kk % NA);  // A chunk slot
-        if constexpr (V == L) {
+        if constexpr (PART == 2) {
+          // the kept bins of this row, as the y-FFT pass wrote them (slot[q], q < keep)
+          constexpr int QB = V == L ? KP : 2 * KP;  // bins per lane
+          float2 o[QB];
+#pragma unroll
+          for (int k2 = 0; k2 < QB; ++k2) {
+            const int q = V == L ? lane + L * k2 : (lane >> 1) + 8 * k2;
+            o[k2] = (q < keep && (V == L || (k2 & 1) == (lane & 1))) ? slot[q] : make_float2(0.f, 0.f);
+          }
+          __syncwarp(tmask);
+          if (lane == 0) mbar_arrive(&empty[b]);
+          if (kk >= NA) mbar_wait(&aempty[s], (uint32_t)(((kk / NA) - 1) & 1));
+#pragma unroll
+          for (int k2 = 0; k2 < QB; ++k2) {
+            if (V != L && (k2 & 1) != (lane & 1)) continue;
+            const int q = V == L ? lane + L * k2 : (lane >> 1) + 8 * k2;
+            put_a<G::AW>(As, s * KC * KT + team * KT + q, q < keep ? o[k2] : make_float2(0.f, 0.f));
+          }
+        } else if constexpr (V == L) {
         float2 v[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) v[j] = slot[lane + L * j];
@@ -435,7 +459,11 @@ __global__ void __launch_bounds__(640, 1) fused1d_kernel(FusedArgs a) {
       };
       for (int n = cr * NC + team; n < (cr + 1) * NC; n += TEAMS) {
         float2* dst = yg + (int64_t)n * a.y_sn;
-        if constexpr (V == L) {
+        if constexpr (PART == 1) {
+          // K4: the unscaled C row (first keep bins) for the separate padded y-iFFT pass
+          float2* cdst = a.C + bb * a.c_sb + pp * a.c_sp + (n0 + n) * a.c_sn;
+          for (int q = lane; q < keep; q += L) __stcs(cdst + q, cval(n, q));
+        } else if constexpr (V == L) {
         float2 xk[KP];
 #pragma unroll
         for (int k2 = 0; k2 < KP; ++k2) {
@@ -525,14 +553,14 @@ static const F1Shape* f1_pick(int n, int keep, int H, int NO) {
 
 bool fused1d_supported(int n, int keep, int H, int NO) { return f1_pick(n, keep, H, NO) != nullptr; }
 
-template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS>
+template <int L, int V, int KP, int TI, int TJ, int NOUT, int CS, int PART = 0>
 static cudaError_t launch_f1(const FusedArgs& a, cudaStream_t s) {
   using G = F1Geo<L, V, KP, TI, TJ, NOUT>;
   static_assert(G::smem_bytes() <= 227 * 1024, "shared memory");
   const size_t smem = G::smem_bytes();
   if ((uintptr_t)a.x % 16 || (uintptr_t)a.W % 16 || (a.x_sh % 2) || (a.x_sb % 2) || (a.x_sp % 2))
     return cudaErrorNotSupported;  // TMA bulk copies need 16-byte aligned rows
-  auto kern = fused1d_kernel<L, V, KP, TI, TJ, NOUT, CS>;
+  auto kern = fused1d_kernel<L, V, KP, TI, TJ, NOUT, CS, PART>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -619,6 +647,8 @@ cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s) {
   if (!p) return cudaErrorNotSupported;
 #define F1_CASE(LL, VV, KK, TI_, TJ_, NO_)                                                          \
   if (p->L == LL && p->V == VV && p->KP == KK && p->NOUT == NO_) {                                  \
+    if (a.part == 1) return CS == 1 ? launch_f1<LL, VV, KK, TI_, TJ_, NO_, 1, 1>(a, s) : cudaErrorNotSupported; \
+    if (a.part == 2) return CS == 1 ? launch_f1<LL, VV, KK, TI_, TJ_, NO_, 1, 2>(a, s) : cudaErrorNotSupported; \
     if (CS == 4) return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 4>(a, s);                             \
     if (CS == 2) return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 2>(a, s);                             \
     return launch_f1<LL, VV, KK, TI_, TJ_, NO_, 1>(a, s);                                          \

@@ -54,6 +54,7 @@ struct FusedArgs {
   int NT, KC, EC;
   int nsplit;  // fused1d: output channels split over nsplit CTAs per row group (forward recomputed)
   int cluster;  // fused1d: hidden channels split over a cluster of CTAs, partial C reduced over DSMEM
+  int part;     // fused1d: 0 full layer, 1 FFT + GEMM -> C (K4), 2 A -> GEMM + iFFT (K5)
   const float2* twg;
   float inv_scale;
 };

@@ -166,3 +166,18 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=root, TFNO_TINY1D="0"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode", ["fused_fft_gemm", "fused_gemm_ifft"])
+@pytest.mark.parametrize("case", [c for c in CASES if c[6] % 2 == 0])
+def test_fused1d_partial_modes(T, O, case, mode):
+    """K4 (fused_fft_gemm: the fused kernel's FFT + GEMM half writes C, then the
+    padded y-iFFT pass) and K5 (fused_gemm_ifft: the y-FFT pass writes A, the
+    kernel's GEMM + iFFT half reads it) vs the oracle of the same mode."""
+    cfg = T.FnoLayerConfig(*case)
+    sched = T.layer_schedule(cfg, mode)[1]
+    assert "fused1d" in sched, sched
+    x, w = O.random_inputs(cfg, 5000 + sum(case))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode=mode)
+    err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w, mode))
+    assert err < FP32_TOL, (case, mode, err)

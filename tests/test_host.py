@@ -120,7 +120,8 @@ def test_schedules_and_workspace():
     assert T.layer_schedule(c1, "fully_fused") == (1, "tiny1d-fft-cgemm-ifft")  # one launch (tiny1d.cu)
     assert T.layer_schedule(T.FnoLayerConfig(256, 64, 64, 1, 128, 1, 32, 1), "fully_fused") == \
         (1, "fused1d-fft-cgemm-ifft")  # more CTAs than one wave: the persistent fused kernel
-    assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused-fft-cgemm|y-ifft")
+    assert T.layer_schedule(c1, "fused_fft_gemm") == (2, "fused1d-fft-cgemm|y-ifft")  # K4 on the fused 1D kernel
+    assert T.layer_schedule(c1, "fused_gemm_ifft") == (2, "y-fft|fused1d-cgemm-ifft")  # K5
     c2 = T.FnoLayerConfig(1024, 256, 256, 1, 256, 1, 32, 1)
     assert T.layer_schedule(c2, "fully_fused") == (1, "fused1d-fft-cgemm-ifft")
     c2b = T.FnoLayerConfig(1024, 256, 256, 1, 4096, 1, 512, 1)

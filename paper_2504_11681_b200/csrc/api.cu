@@ -172,10 +172,13 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
   }
   bool want_fg = (mode == TFNO_FUSED_FFT_GEMM || mode == TFNO_FULLY_FUSED);
   bool want_gi = (mode == TFNO_FUSED_GEMM_IFFT || mode == TFNO_FULLY_FUSED);
-  if (g.rank == 2 && mode == TFNO_FULLY_FUSED && plane2d_supported(c)) {
+  // rank 2 on the per-plane kernels: fully_fused, and fused_gemm_ifft as the fused channel mix +
+  // inverse kernel (the GEMM-iFFT fusion of the mode, plane_invmix_g)
+  if (g.rank == 2 && plane2d_supported(c) &&
+      (mode == TFNO_FULLY_FUSED || (mode == TFNO_FUSED_GEMM_IFFT && plane2d_fusedmix(c, prec, mode)))) {
     s.plane2d = true;
     s.need_A = s.need_C = true;
-    if (plane2d_fusedmix(c, prec)) {
+    if (plane2d_fusedmix(c, prec, mode)) {
       s.plane_mix = true;
       s.launches = 2;
       s.desc = "plane-fft2d|plane-mix-ifft2d";
@@ -469,7 +472,7 @@ size_t base_ws_bytes(const tfno_cfg* c, int mode, int prec) {  // intermediates 
   if (s.need_mid) e += g.B * g.N * g.kx * g.dy;
   const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;  // generic plane kernels: KP^2 padded modes
   if (s.need_A) e += g.B * g.H * mq;
-  if (s.need_C) e += s.plane2d ? plane2d_c_elems(c, prec) : g.B * g.N * mq;
+  if (s.need_C) e += s.plane2d ? plane2d_c_elems(c, prec, mode) : g.B * g.N * mq;
   return e * sizeof(float2);
 }
 
@@ -779,7 +782,7 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
   if (s.need_mid) { mid = p; p += g.B * g.N * g.kx * g.dy; }
   const int64_t mq = s.plane2d ? plane2d_modes(c) : g.kx * g.ky;
   if (s.need_A) { A = p; p += g.B * g.H * mq; }
-  if (s.need_C) { Cm = p; p += s.plane2d ? plane2d_c_elems(c, prec) : g.B * g.N * mq; }
+  if (s.need_C) { Cm = p; p += s.plane2d ? plane2d_c_elems(c, prec, mode) : g.B * g.N * mq; }
   // W' image: the caller's packed weights (tfno_prepare_weights) or built per call in the workspace tail
   const int wimg_ready = (packed && wimg_need) ? 1 : 0;
   void* wimg = wimg_ready ? const_cast<void*>(packed)
@@ -787,7 +790,7 @@ static int layer_forward_impl(const tfno_cfg* c, int mode, int prec, const void*
 
   stage_begin(st);
   if (s.plane2d)
-    return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, wimg_ready, st, &stage_mark));
+    return cuda_status(launch_plane2d_layer(c, x, w, y, A, Cm, tw, prec, wimg, wimg_ready, st, &stage_mark, mode));
   if (s.tiny) {
     const cudaError_t te = launch_tiny1d(x, w, y, (int)g.dy, (int)g.B, (int)g.H, (int)g.N, (int)g.ky, tw, st);
     if (te == cudaSuccess) stage_mark(st);

@@ -714,13 +714,15 @@ static int plane_fusedmix_env() {  // TFNO_PLANE_FUSEDMIX=0/1 overrides the per-
   return v;
 }
 
-bool plane2d_fusedmix(const tfno_cfg* c, int prec) {
+bool plane2d_fusedmix(const tfno_cfg* c, int prec, int mode) {
   // FP32: SIMT mix warps; TF32 / 3xTF32: tcgen05 mix (BF16 keeps the standalone kind::f16 contraction)
   if ((prec != TFNO_FP32 && prec != TFNO_TF32 && prec != TFNO_TF32X3) || !plane2d_supported(c)) return false;
   if ((int64_t)c->batch * ((c->output_dim + 7) / 8) > (1LL << 40)) return false;
   const int env = plane_fusedmix_env();
   if (env == 0 || plane_g_invmix_smem(c, prec) == 0) return false;
   if (env == 1) return true;
+  // fused_gemm_ifft asks for exactly this fusion (channel mix + inverse in one kernel)
+  if (mode == TFNO_FUSED_GEMM_IFFT) return prec == TFNO_FP32;
   // the tcgen05 mix inside the inverse is opt-in (TFNO_PLANE_FUSEDMIX=1): its A staging
   // (global -> registers -> canonical K-major tiles, one K step per chunk) keeps too few
   // loads in flight -- measured (profiles/r02/tcmix_ab.txt) C4 3xTF32 mix + inverse 8.08 ms
@@ -735,9 +737,9 @@ bool plane2d_fusedmix(const tfno_cfg* c, int prec) {
   return (int64_t)c->hidden_dim * c->output_dim >= 128 * 128 && tasks >= 8LL * device_sms();
 }
 
-int64_t plane2d_c_elems(const tfno_cfg* c, int prec) {
+int64_t plane2d_c_elems(const tfno_cfg* c, int prec, int mode) {
   const int64_t mq = plane2d_modes(c);
-  if (plane2d_fusedmix(c, prec)) return (int64_t)device_sms() * 2 * kMixGNHost * mq;
+  if (plane2d_fusedmix(c, prec, mode)) return (int64_t)device_sms() * 2 * kMixGNHost * mq;
   return (int64_t)c->batch * c->output_dim * mq;
 }
 
@@ -808,10 +810,10 @@ cudaError_t launch_plane2d_inv(const tfno_cfg* c, const float2* modes, float2* y
 
 cudaError_t launch_plane2d_layer(const tfno_cfg* c, const float2* x, const float2* w, float2* y, float2* A,
                                  float2* Cm, const float2* tw, int prec, void* wimg, int wimg_ready,
-                                 cudaStream_t st, void (*mark)(cudaStream_t)) {
+                                 cudaStream_t st, void (*mark)(cudaStream_t), int mode) {
   const int64_t B = c->batch, H = c->hidden_dim, N = c->output_dim;
   const int mix = plane_mix(c);
-  if (plane2d_fusedmix(c, prec)) {
+  if (plane2d_fusedmix(c, prec, mode)) {
     // forward in the natural mode order the generic inverse reads, then the
     // channel mix + inverse in one kernel (C stays in the per-CTA L2 ring Cm)
     cudaError_t e = (mix & 1) ? plane_g_run(c, -1, x, A, B * H, tw, 1.0f, st) : tuned_fwd(c, x, A, B * H, tw, true, st);

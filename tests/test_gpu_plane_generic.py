@@ -185,3 +185,16 @@ def test_generic_plane_spectrum_api(T, O, shape):
     spec = np.zeros((B, H, dx, dy), np.complex128)
     spec[:, :, :kx, :ky] = want
     assert T.max_rel_error(back.cpu().numpy(), np.fft.ifft2(spec)) < FP32_TOL
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 13, 512, 512, 64, 64), (3, 5, 9, 256, 256, 32, 32), (4, 6, 7, 128, 256, 20, 12),
+                                   (2, 4, 4, 256, 256, 16, 16)], ids=_ids)
+def test_plane_fused_gemm_ifft_mode(T, O, shape):
+    """mode fused_gemm_ifft on rank-2 planes = plane forward + the fused channel
+    mix / inverse kernel (the GEMM-iFFT fusion), vs the oracle of that mode."""
+    B, H, N, dx, dy, kx, ky = shape
+    cfg = T.FnoLayerConfig(B, H, N, dx, dy, kx, ky, rank=2)
+    assert T.layer_schedule(cfg, "fused_gemm_ifft")[1] == "plane-fft2d|plane-mix-ifft2d"
+    x, w = O.random_inputs(cfg, 60 + sum(shape))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fused_gemm_ifft")
+    assert T.max_rel_error(out.data, O.run_layer_values(cfg, x, w, "fused_gemm_ifft")) < FP32_TOL

@@ -134,6 +134,8 @@ def test_schedules_and_workspace():
     assert T.workspace_bytes(r3, "fully_fused") == 2 * (16 + 8) * 32 * 32 * 8
     c3 = T.FnoLayerConfig(32, 64, 64, 256, 256, 32, 32, 2)  # too few mix tasks per CTA: standalone CGEMM
     assert T.layer_schedule(c3, "fully_fused") == (3, "plane-fft2d|cgemm-modes|plane-ifft2d")
+    # fused_gemm_ifft on the plane path is the fused channel mix + inverse kernel
+    assert T.layer_schedule(c3, "fused_gemm_ifft") == (2, "plane-fft2d|plane-mix-ifft2d")
     r4 = T.FnoLayerConfig(2, 16, 16, 64, 32, 8, 16, 2)  # dy < 64: the paper schedule
     assert T.layer_schedule(r4, "fully_fused") == (3, "x-fft|fused-fft-cgemm-ifft|x-ifft")
     f = T.layer_flops(c4)

@@ -154,6 +154,13 @@ int tfno_cgemm_prec(int64_t M, int64_t N, int64_t K, int64_t batch, const void* 
  * reduction of the per-element grad_W partials of the backward pass (extension). */
 int tfno_batch_sum(const void* in, int64_t batch, int64_t n, void* out, void* stream);
 
+/* Per-mode channel mix (extension: per-mode weights, einsum bhq,hnq->bnq):
+ * C[b][n][q] = alpha * sum_h A[b][h][q] * W[h][n][q], complex64, q < modes fastest in all three
+ * (A = the truncated spectrum [batch][hidden][kx*ky], W = [hidden][out][kx][ky] weights,
+ * C = the modes the padded inverse reads).  FP32 accumulation in ascending h. */
+int tfno_permode_mix(int64_t batch, int64_t hidden, int64_t out, int64_t modes, const void* A, const void* W,
+                     void* C, float alpha, void* stream);
+
 /* Plane modulation (symmetric +-mode truncation, an extension beyond the reference):
  * out[p][x][y] = scale * in[p][x][y] * exp(sign * 2*pi*i * (sx*x/dx + sy*y/dy)), sign = +1 / -1.
  * Modulating by (+keep_x/2, +keep_y/2) before and (-keep_x/2, -keep_y/2) after the first-keep

@@ -59,6 +59,7 @@ _SIGS = {
     "tfno_cgemm_prec": (ctypes.c_int, [_I64, _I64, _I64, _I64, _VP, _I64, _I64, _I64, _VP, _I64, _I64, _I64,
                                        _VP, _I64, _I64, _I64, ctypes.c_float, ctypes.c_int, _VP]),
     "tfno_batch_sum": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP]),
+    "tfno_permode_mix": (ctypes.c_int, [_I64, _I64, _I64, _I64, _VP, _VP, _VP, ctypes.c_float, _VP]),
     "tfno_modulate": (ctypes.c_int, [_I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      _VP, _VP, ctypes.c_float, _VP]),
     "tfno_real_to_complex": (ctypes.c_int, [_VP, _VP, _I64, _VP]),

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--cudart
               "-Xptxas", "-v"] + ARCH
 # (source, extra nvcc flags, object name): plane_g.cu is built once per row length
 PLANE_G = [("plane_g.cu", ["-DPLANE_G_DY=%d" % d], "plane_g_%d.cu.o" % d) for d in (64, 128, 256, 512, 1024)]
-SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "warpfft_fwd.cu", "fused1d.cu", "tiny1d.cu", "realfield.cu", "api.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "plane2d.cu", "rows1d.cu", "cgemm_tc.cu", "warpfft.cu", "warpfft_fwd.cu", "fused1d.cu", "tiny1d.cu", "permode.cu", "realfield.cu", "api.cu", "plan.cpp"]
 
 
 def _nvcc() -> str:

@@ -621,6 +621,15 @@ int tfno_batch_sum(const void* in, int64_t batch, int64_t n, void* out, void* st
   return cuda_status(launch_batch_sum((const float2*)in, batch, n, (float2*)out, (cudaStream_t)stream));
 }
 
+int tfno_permode_mix(int64_t batch, int64_t hidden, int64_t out, int64_t modes, const void* A, const void* W,
+                     void* C, float alpha, void* stream) {
+  if (batch < 0 || hidden < 0 || out < 0 || modes < 0) return TFNO_EINVAL;
+  if (batch == 0 || out == 0 || modes == 0) return TFNO_OK;
+  if (!A || !W || !C) return TFNO_EINVAL;
+  return cuda_status(launch_permode_mix((const float2*)A, (const float2*)W, (float2*)C, batch, hidden, out, modes,
+                                        alpha, (cudaStream_t)stream));
+}
+
 int tfno_modulate(int64_t planes, int dx, int dy, int sx, int sy, int sign, const void* in, void* out, float scale,
                   void* stream) {
   if (planes < 0 || !pow2(dx) || !pow2(dy) || dx > TFNO_TW_MAX || dy > TFNO_TW_MAX || (sign != 1 && sign != -1))

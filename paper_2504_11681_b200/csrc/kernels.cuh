@@ -80,6 +80,9 @@ inline cudaError_t launch_cgemm_prec(const GemmArgs& g, int prec, cudaStream_t s
   return cudaErrorNotSupported;
 }
 cudaError_t launch_fused(const FusedArgs& a, bool fuse_fft, bool fuse_ifft, cudaStream_t s);
+// per-mode channel mix C[b][n][q] = alpha sum_h A[b][h][q] W[h][n][q] (permode.cu)
+cudaError_t launch_permode_mix(const float2* A, const float2* W, float2* C, int64_t B, int64_t H, int64_t N,
+                               int64_t MQ, float alpha, cudaStream_t s);
 cudaError_t launch_batch_sum(const float2* in, int64_t batch, int64_t n, float2* out, cudaStream_t s);
 cudaError_t launch_modulate(const float2* in, float2* out, int64_t planes, int dx, int dy, int sx, int sy, int sign,
                             float scale, const float2* tw, cudaStream_t s);

@@ -7,10 +7,10 @@ extension is pinned by its own float64 oracle (``tests/test_gpu_permode.py``).
 Same first-``keep``-bin truncation, zero padding and 1/(dx*dy) inverse as the
 reference layer; the transforms are the sm_100a spectrum kernels of the
 forward path (per-plane 2D kernels for the plane shapes, row/pencil FFTs
-otherwise) and the channel mix is the FP32 SIMT mode CGEMM batched over the
-kx*ky modes (M = batch, K = H, N = N_out) on mode-major copies of the
-spectra.  Mode-major weights are prepared once per weight tensor
-(``prepare_weights``).
+otherwise) and the channel mix is ``tfno_permode_mix`` (csrc/permode.cu): a
+mode-parallel FP32 contraction that reads the spectrum [B][H][kx*ky] and the
+weights [H][N][kx][ky] in their natural layouts and writes the [B][N][kx][ky]
+modes the inverse consumes, so there are no mode-major copies on the path.
 """
 
 from __future__ import annotations
@@ -18,13 +18,14 @@ from __future__ import annotations
 from . import _device
 from ._lib import check, lib
 from .core import FnoLayerConfig, ShapeMismatch
-from .multigpu import spectrum_forward, spectrum_inverse
+from .multigpu import _on, spectrum_forward, spectrum_inverse
 
 
 def prepare_weights(w_modes):
-    """[H, N, kx, ky] complex64 (CUDA) -> mode-major [kx*ky, H, N] contiguous."""
+    """[H, N, kx, ky] complex64 (CUDA) -> the contiguous [H, N, kx*ky] the mix kernel reads
+    (a no-op view for contiguous complex64 weights)."""
     H, N, kx, ky = w_modes.shape
-    return w_modes.permute(2, 3, 0, 1).reshape(kx * ky, H, N).contiguous()
+    return w_modes.to(_device.torch().complex64).reshape(H, N, kx * ky).contiguous()
 
 
 def run_layer_permode(cfg: FnoLayerConfig, x, w_modes=None, w_prepared=None, stream=None):
@@ -42,12 +43,15 @@ def run_layer_permode(cfg: FnoLayerConfig, x, w_modes=None, w_prepared=None, str
         if w_modes is None or tuple(w_modes.shape) != (H, N, kx, ky):
             raise ShapeMismatch(f"w_modes must be [{H}, {N}, {kx}, {ky}]")
         w_prepared = prepare_weights(w_modes)
+    if (tuple(w_prepared.shape) != (H, N, MQ) or not w_prepared.is_contiguous()
+            or w_prepared.dtype != t.complex64):
+        raise ShapeMismatch(f"w_prepared must be a contiguous complex64 [{H}, {N}, {MQ}] tensor (prepare_weights)")
     A = spectrum_forward(cfg, x.contiguous(), stream)                  # [B,H,kx,ky]
-    Aq = A.reshape(B, H, MQ).permute(2, 1, 0).contiguous()             # [q][h][b]
-    Cq = t.empty((MQ, N, B), dtype=t.complex64, device=x.device)       # [q][n][b]
-    # per mode q: C[q] (B x N, b fastest) = A[q]^T (B x H) * W[q] (H x N)
-    rc = lib().tfno_cgemm(B, N, H, MQ, Aq.data_ptr(), 1, B, H * B, w_prepared.data_ptr(), N, 1, H * N,
-                          Cq.data_ptr(), 1, B, N * B, 1.0, _device.stream_ptr(stream))
-    check(rc, "tfno_cgemm")
-    C = Cq.permute(2, 1, 0).reshape(B, N, kx, ky).contiguous()         # [B,N,kx,ky]
+    with _on(stream):
+        C = t.empty((B, N, kx, ky), dtype=t.complex64, device=x.device)
+    # C[b][n][q] = sum_h A[b][h][q] W[h][n][q]
+    rc = lib().tfno_permode_mix(B, H, N, MQ, A.data_ptr(), w_prepared.data_ptr(), C.data_ptr(), 1.0,
+                                _device.stream_ptr(stream))
+    check(rc, "tfno_permode_mix")
     return spectrum_inverse(cfg, C, (B, N), scale=1.0, stream=stream)
+

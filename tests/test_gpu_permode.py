@@ -25,7 +25,10 @@ CASES = [
     (64, 8, 6, 1, 256, 1, 32, 1),        # 1D, mode CGEMM fast path (M = batch = 64)
     (5, 4, 3, 1, 128, 1, 20, 1),         # 1D, general CGEMM (small batch, ragged keep)
     (2, 4, 5, 64, 64, 8, 8, 2),          # 2D generic spectra
-    (128, 4, 4, 256, 256, 32, 32, 2),    # 2D plane kernels, fast mode CGEMM (batch 128)
+    (128, 4, 4, 256, 256, 32, 32, 2),    # 2D plane kernels (batch 128)
+    (19, 7, 21, 1, 128, 1, 37, 1),       # ragged batch / channels / modes (every tile edge masked)
+    (3, 9, 5, 128, 64, 9, 7, 2),         # 2D ragged keeps: 63 modes
+    (40, 70, 33, 64, 64, 16, 16, 2),     # H not a multiple of the 4-deep chunk, several b / n tiles
 ]
 
 
@@ -42,10 +45,11 @@ def test_permode_vs_float64(case):
                                           generator=g))
     y = run_layer_permode(cfg, x.cuda(), w.cuda())
     y2 = run_layer_permode(cfg, x.cuda(), w_prepared=prepare_weights(w.cuda()))
+    y3 = run_layer_permode(cfg, x.cuda(), w.cuda())
     torch.cuda.synchronize()
     ref = _ref(x, w, cfg)
     assert T.max_rel_error(y.cpu().numpy(), ref.numpy()) < TOL
-    assert torch.equal(y, y2)
+    assert torch.equal(y, y2) and torch.equal(y, y3)  # deterministic
 
 
 def test_permode_equals_shared_weights_when_modes_repeat():
@@ -61,3 +65,24 @@ def test_permode_equals_shared_weights_when_modes_repeat():
     y2 = T.run_layer_device(cfg, x, w)
     torch.cuda.synchronize()
     assert T.max_rel_error(y1.cpu().numpy(), y2.cpu().numpy()) < TOL
+
+
+def test_permode_mix_abi_vs_einsum():
+    """tfno_permode_mix straight through the C-ABI: C = alpha * einsum(bhq,hnq->bnq) in float64,
+    natural layouts, alpha applied, zero-size problems are no-ops, bad sizes are rejected."""
+    import torch
+
+    import paper_2504_11681_b200 as T
+    from paper_2504_11681_b200._lib import lib
+    g = torch.Generator().manual_seed(3)
+    for B, H, N, MQ in [(17, 13, 35, 100), (64, 128, 16, 32), (1, 1, 1, 1)]:
+        A = torch.view_as_complex(torch.randn((B, H, MQ, 2), generator=g))
+        W = torch.view_as_complex(torch.randn((H, N, MQ, 2), generator=g))
+        C = torch.empty((B, N, MQ), dtype=torch.complex64, device="cuda")
+        Ad, Wd = A.cuda(), W.cuda()
+        assert lib().tfno_permode_mix(B, H, N, MQ, Ad.data_ptr(), Wd.data_ptr(), C.data_ptr(), 0.5, None) == 0
+        torch.cuda.synchronize()
+        ref = 0.5 * torch.einsum("bhq,hnq->bnq", A.to(torch.complex128), W.to(torch.complex128))
+        assert T.max_rel_error(C.cpu().numpy(), ref.numpy()) < TOL
+    assert lib().tfno_permode_mix(0, 3, 3, 3, None, None, None, 1.0, None) == 0
+    assert lib().tfno_permode_mix(-1, 3, 3, 3, None, None, None, 1.0, None) != 0

@@ -226,11 +226,14 @@ Sched make_sched(const tfno_cfg* c, int mode, int prec = 0, bool allow_f1 = true
   // the partial fusions (K4 fused_fft_gemm / K5 fused_gemm_ifft) on the same kernel: its FFT + GEMM
   // half writing C, or its GEMM + iFFT half reading the y-FFT's A (even keep: 16-byte bulk rows)
   const bool part_mode = mode == TFNO_FUSED_FFT_GEMM || mode == TFNO_FUSED_GEMM_IFFT;
-  if (allow_f1 && part_mode && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1) && g.ky % 2 == 0) {
+  const int gi_split = mode == TFNO_FUSED_GEMM_IFFT
+                           ? fused1d_split_gemm_ifft((int)g.dy, (int)g.ky, (int)g.H, (int)g.N) : 0;
+  if (allow_f1 && part_mode && f1_env != 0 && !tc_heavy && (f1_full || f1_forced > 1 || gi_split > 1) &&
+      g.ky % 2 == 0) {
     s.f1 = true;
     s.f1_part = mode == TFNO_FUSED_FFT_GEMM ? 1 : 2;
     s.f1_cluster = 1;
-    s.f1_split = f1_full ? 1 : f1_forced;
+    s.f1_split = f1_full ? 1 : (s.f1_part == 2 ? std::max(gi_split, f1_forced) : f1_forced);
     s.fg = s.f1_part == 1;
     s.gi = s.f1_part == 2;
     s.need_s1 = s.need_mid = (g.rank == 2);

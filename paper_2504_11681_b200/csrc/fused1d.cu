@@ -623,6 +623,15 @@ int fused1d_split(int n, int keep, int H, int NO, int64_t G) {
   return S;
 }
 
+// K5 (GEMM + padded iFFT from the y-FFT's A): splitting the output channels recomputes nothing
+// (each split item streams the same A rows), so any batch may split until the C tile fits
+int fused1d_split_gemm_ifft(int n, int keep, int H, int NO) {
+  if (f1_pick(n, keep, H, NO)) return 1;
+  for (int S = 2; S <= 8; S *= 2)
+    if (NO % S == 0 && f1_pick(n, keep, H, NO / S)) return S;
+  return 0;
+}
+
 int fused1d_cluster(int n, int keep, int H, int NO, int64_t G) {
   static int env = -2;
   if (env == -2) {

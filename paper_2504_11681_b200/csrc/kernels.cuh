@@ -96,6 +96,7 @@ bool warp_fused_supported(int n, int keep, int H, int NO);
 bool fused1d_supported(int n, int keep, int H, int NO);
 // output-channel split for fused1d so that small batches still fill the SMs (0 = unsupported)
 int fused1d_split(int n, int keep, int H, int NO, int64_t G);
+int fused1d_split_gemm_ifft(int n, int keep, int H, int NO);  // K5: output-channel split, any batch (0: none)
 // hidden-channel cluster split for fused1d (0/1 = none); takes precedence over the output split
 int fused1d_cluster(int n, int keep, int H, int NO, int64_t G);
 cudaError_t launch_fused1d(const FusedArgs& a, cudaStream_t s);

@@ -181,3 +181,18 @@ def test_fused1d_partial_modes(T, O, case, mode):
     out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode=mode)
     err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w, mode))
     assert err < FP32_TOL, (case, mode, err)
+
+
+@pytest.mark.parametrize("case", [(3, 128, 128, 1, 1024, 1, 128, 1), (100, 256, 256, 1, 1024, 1, 128, 1),
+                                  (2, 256, 256, 1, 1024, 1, 96, 1), (5, 128, 512, 1, 1024, 1, 128, 1),
+                                  (80, 96, 128, 1, 1024, 1, 128, 1)])
+def test_fused_gemm_ifft_channel_split(T, O, case):
+    """K5 where the full C tile does not fit one CTA (N = 1024 with 128+ output
+    channels): the output channels are split across items at any batch (each
+    split streams the same A rows, nothing is recomputed) — vs the oracle."""
+    cfg = T.FnoLayerConfig(*case)
+    assert T.layer_schedule(cfg, "fused_gemm_ifft")[1] == "y-fft|fused1d-cgemm-ifft"
+    x, w = O.random_inputs(cfg, 7000 + sum(case))
+    out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fused_gemm_ifft")
+    err = T.max_rel_error(out.data, O.run_layer_values(cfg, x, w, "fused_gemm_ifft"))
+    assert err < FP32_TOL, (case, err)

@@ -24,7 +24,15 @@ struct PGCfg {
   static constexpr int CAPF = KP >= 128 ? 128 : 256;
   static constexpr int NTHF = M * (KP < CAPF / M ? KP : CAPF / M);
   static constexpr int NTHI = M * (KP < 256 / M ? KP : 256 / M);
-  static constexpr int S = KP >= 128 ? 2 : 3;
+  // 512^2 / keep 64 (C4): a 4-slot ring with the class accumulators in registers beats
+  // 3 slots with shared-memory accumulators (same box, alternating: 14.10 / 14.21 ->
+  // 13.98 / 14.06 ms per C4 layer, profiles/r02/s4_ab.txt); -DTFNO_PG_S3 restores it
+#ifndef TFNO_PG_S3
+  static constexpr bool S4 = DY == 512 && KP == 64;
+#else
+  static constexpr bool S4 = false;
+#endif
+  static constexpr int S = S4 ? 4 : KP >= 128 ? 2 : 3;
   static constexpr bool BIG = KP >= 128;  // accumulate classes in global, mode tile read from L2
   using GF = PG<DY, KP, KP, NTHF>;
   using GI = PG<DY, KP, KP, NTHI>;
@@ -33,7 +41,7 @@ struct PGCfg {
   static constexpr size_t FWD_BASE = sizeof(float2) * ((size_t)S * GF::TEAMS * DY + (size_t)GF::NTB * GF::TB +
                                                        (size_t)KP * KP + DY + KP + 1024) + 16 * S + 16;
   static constexpr size_t ACC_BYTES = sizeof(float2) * (size_t)GF::TASKS2 * GF::KA * GF::NTH;
-  static constexpr bool ACCS = !BIG && FWD_BASE + ACC_BYTES <= 227 * 1024;
+  static constexpr bool ACCS = !S4 && !BIG && FWD_BASE + ACC_BYTES <= 227 * 1024;
 };
 
 template <class G>

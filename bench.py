@@ -397,7 +397,9 @@ def run_ours(args):
     nlayers = LAYERS.get(args.workload, 1)
     chain = None
     io_bytes = 8 * B * (H + N) * dx * dy
-    use_graph = nlayers > 1 or args.graph == "on" or (args.graph == "auto" and io_bytes < (256 << 20))
+    # auto: chains, and layers whose step is short enough (<= 4 GiB of I/O, < ~1 ms) that the
+    # eager launch + stage-event gaps show (C3 0.443 -> 0.425 ms, profiles/r02/c3_graph_pdl.txt)
+    use_graph = nlayers > 1 or args.graph == "on" or (args.graph == "auto" and io_bytes <= (4 << 30))
     if use_graph:  # launch-latency-bound workloads (and chains) replay one CUDA graph per step
         from paper_2504_11681_b200.chain import FnoChain
         ws_ = [w] + [torch.view_as_complex(torch.randn((H, N, 2), generator=g, device=dev,
@@ -734,7 +736,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="time CUDA-graph replays of the layer (auto: chains and workloads < 256 MiB of I/O)")
+                    help="time CUDA-graph replays of the layer (auto: chains and workloads <= 4 GiB of I/O)")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -87,7 +87,16 @@ constexpr int kComputeBar = 15;
 // Warp-specialised: warp NTH/32 is the TMA producer (ring of S slots, full /
 // empty mbarriers); the NTH compute threads form row teams that synchronise
 // only inside the team, plus one compute-wide barrier per class (column pass).
-template <class G, int S, bool NATURAL, bool DLD>
+// SKEW: the class tail is software-pipelined over three class buffers — in the
+// iteration that runs the rows of class c, threads [NTH - KA*KY, NTH) run the
+// column pass 1 of class c-1 and threads [0, 8*KY) the pass 2 + accumulation of
+// class c-2, then ONE compute-wide barrier (instead of three per class with 3/4
+// or 1/2 of the threads idle between them).  Same operations in the same order:
+// bitwise-identical modes.
+template <class G>
+__host__ __device__ constexpr bool fwd_skew_ok() { return 8 * G::KY + (G::KX / 8) * G::KY <= G::NTH; }
+
+template <class G, int S, bool NATURAL, bool DLD, bool SKEW = false>
 __global__ void __launch_bounds__(G::NTH + 32, 1)
     plane_fwd2d_kernel(const float2* __restrict__ x, float2* __restrict__ Aout, int64_t planes,
                        const float2* __restrict__ twg) {
@@ -95,19 +104,24 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
   constexpr int RT = G::RT, RS = G::RS, RPT = G::RPT, ROWS = G::ROWS;
   static_assert(RPT == 1 || !DLD, "direct loads only with one row per team");
+  static_assert(!SKEW || fwd_skew_ok<G>(), "skewed tail: disjoint pass-1 / pass-2 thread ranges");
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ring = reinterpret_cast<float2*>(smem);
   float2* tr = ring + (DLD ? 0 : S * ROWS * NY);  // DLD: rows go straight to registers (no ring)
   float2* red = tr + ROWS * 8 * TS;
-  float2* Tc = red + ROWS * 8 * RS;
-  float2* twy = Tc + KX * KY;
-  float2* twx = twy + NY;
+  float2* const Tc0 = red + ROWS * 8 * RS;
+  // SKEW: the row twiddle table (read into registers once, before any row) aliases
+  // class buffer 2, first written by the rows of class 2, two barriers later
+  static_assert(!SKEW || NY <= KX * KY, "twy alias");
+  float2* twy = SKEW ? Tc0 + 2 * KX * KY : Tc0 + KX * KY;
+  float2* twx = SKEW ? Tc0 + 3 * KX * KY : twy + NY;
   uint64_t* full = reinterpret_cast<uint64_t*>(twx + DX);
   uint64_t* empty = full + S;
 
   const int tid = threadIdx.x;
   const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t NIT = nmine * R * IPC;
+  const int64_t NCL = nmine * R;  // classes of this CTA
 
   for (int k = tid; k < NY; k += blockDim.x) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / NY)]);
   for (int k = tid; k < DX; k += blockDim.x) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)]);
@@ -192,12 +206,56 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   }
   // nested (plane, class, row-group) loops, ring slot / phase kept incrementally
   // (no 64-bit index divisions): C4 forward 6.98 -> 6.67 ms on one box
+  // SKEW: pass 1 of class c-1 (threads [NTH - KA*KY, NTH)) and pass 2 of class c-2
+  // (threads [0, 8*KY)) on their own class buffers, then the one barrier per class
+  auto skew_tail = [&](int64_t c) {
+    if (c >= 1 && c - 1 < NCL) {
+      const int tau = tid - (NTH - KA * KY);
+      if (tau >= 0) {
+        float2* T1 = Tc0 + (int)((c - 1) % 3) * (KX * KY);
+        const int q = tau % KY, i = tau / KY;
+        float2 v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = T1[(i + KA * m) * KY + q];
+        dft8<-1>(v);
+#pragma unroll
+        for (int s2 = 1; s2 < 8; ++s2) v[s2] = cmul(v[s2], twx[i * s2 * R]);
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) T1[(s2 * KA + i) * KY + q] = v[s2];
+      }
+    }
+    if (c >= 2 && c - 2 < NCL && tid < 8 * KY) {
+      const int64_t c2 = c - 2;
+      const int x0c = (int)(c2 % R);
+      const float2* T2 = Tc0 + (int)(c2 % 3) * (KX * KY);
+      const int q = tid % KY, s2 = tid / KY;
+      float2 w[KA];
+#pragma unroll
+      for (int i = 0; i < KA; ++i) w[i] = T2[(s2 * KA + i) * KY + q];
+      dft_small<KA, -1>(w);
+#pragma unroll
+      for (int u = 0; u < KA; ++u) cmac(acc[0][u], w[u], twx[(s2 + 8 * u) * x0c]);
+      if (x0c == R - 1) {
+        float2* dst = Aout + (blockIdx.x + (c2 / R) * gridDim.x) * (int64_t)KX * KY;
+        const int qo = NATURAL ? (q / T) + 8 * (q % T) : q;
+#pragma unroll
+        for (int u = 0; u < KA; ++u) {
+          dst[(s2 + 8 * u) * KY + qo] = acc[0][u];
+          acc[0][u] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    named_bar(kComputeBar, NTH);
+  };
+
   int it = 0, slot = 0;
   uint32_t phase = 0;
+  int64_t cl = 0;  // class counter (SKEW)
   for (int64_t kp = 0; kp < nmine; ++kp) {
   const int64_t pl = blockIdx.x + kp * gridDim.x;
 #pragma unroll 1
-  for (int x0 = 0; x0 < R; ++x0) {
+  for (int x0 = 0; x0 < R; ++x0, ++cl) {
+  float2* const Tc = SKEW ? Tc0 + (int)(cl % 3) * (KX * KY) : Tc0;
 #pragma unroll 1
   for (int j = 0; j < IPC; ++j, ++it) {
     if (!DLD) mbar_wait(&full[slot], phase);
@@ -290,7 +348,9 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
       phase ^= 1u;
     }
   }  // j: rows of class x0
-    {
+    if constexpr (SKEW) {
+      skew_tail(cl);
+    } else {
       named_bar(kComputeBar, NTH);
       // ---- class x0 complete: kx-point column FFT, pass 1 (radix 8 over m)
       for (int tau = tid; tau < KA * KY; tau += NTH) {
@@ -341,6 +401,10 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
     }
   }  // x0
   }  // planes
+  if constexpr (SKEW) {  // drain: the last two classes' column passes
+    skew_tail(NCL);
+    skew_tail(NCL + 1);
+  }
 }
 
 // ============================================================== inverse
@@ -481,9 +545,9 @@ __global__ void __launch_bounds__(G::NTH, 1)
 
 // ---------------------------------------------------------------- dispatch
 template <class G>
-constexpr size_t fwd_smem(int S, bool dld = false) {
+constexpr size_t fwd_smem(int S, bool dld = false, bool skew = false) {
   return sizeof(float2) * ((size_t)(dld ? 0 : S) * G::ROWS * G::NY + G::ROWS * 8 * (G::TS + G::RS) +
-                           G::KX * G::KY + G::NY + G::DX) +
+                           (skew ? 3 * G::KX * G::KY : G::KX * G::KY + G::NY) + G::DX) +
          16 * S + 64;
 }
 template <class G>
@@ -514,19 +578,36 @@ static int plane_variant() {
 
 static int num_sms() { return device_sms(); }
 
-template <class G, int S, bool NAT, bool DLD>
-static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
+static int plane_skew_env() {  // TFNO_PLANE_SKEW=0 selects the three-barrier class tail (A/B)
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFNO_PLANE_SKEW");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+template <class G, int S, bool NAT, bool DLD, bool SKEW>
+static cudaError_t launch_fwd_k(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
   const int sms = num_sms();
-  size_t smem = fwd_smem<G>(S, DLD);
+  size_t smem = fwd_smem<G>(S, DLD, SKEW);
   int grid = (int)(planes < sms ? planes : sms);
   if (grid < 1) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, NAT, DLD>,
+  cudaError_t e = cudaFuncSetAttribute(plane_fwd2d_kernel<G, S, NAT, DLD, SKEW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(plane_fwd2d_kernel<G, S, NAT, DLD>, dim3(grid), dim3(G::NTH + 32), smem, st, x, A, planes, tw);
+  e = launch_pdl(plane_fwd2d_kernel<G, S, NAT, DLD, SKEW>, dim3(grid), dim3(G::NTH + 32), smem, st, x, A, planes, tw);
   if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
+}
+
+template <class G, int S, bool NAT, bool DLD>
+static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
+  if constexpr (fwd_skew_ok<G>()) {
+    if (plane_skew_env() != 0) return launch_fwd_k<G, S, NAT, DLD, true>(x, A, planes, tw, st);
+  }
+  return launch_fwd_k<G, S, NAT, DLD, false>(x, A, planes, tw, st);
 }
 
 template <class G, int S>
@@ -605,6 +686,8 @@ static bool inv512_half() { return inv_half_env() == 2; }
 using G128 = PlaneGeo<128, 16, 128, 16, 256>;
 
 static_assert(fwd_smem<G512>(3) <= 227 * 1024, "smem");
+static_assert(fwd_smem<G256a>(4, false, true) <= 227 * 1024 && fwd_smem<G256b>(4, false, true) <= 227 * 1024 &&
+                  fwd_smem<G128>(4, false, true) <= 227 * 1024, "smem (skewed tail)");
 static_assert(fwd_smem<G512f>(3) <= 227 * 1024, "smem");
 static_assert(inv_smem<G512>(3) <= 227 * 1024, "smem");
 

@@ -198,3 +198,37 @@ def test_plane_fused_gemm_ifft_mode(T, O, shape):
     x, w = O.random_inputs(cfg, 60 + sum(shape))
     out, _ = T.run_layer(cfg, T.SpectralTensor(x), T.ComplexMatrix(w), mode="fused_gemm_ifft")
     assert T.max_rel_error(out.data, O.run_layer_values(cfg, x, w, "fused_gemm_ifft")) < FP32_TOL
+
+
+_SKEW_CODE = r"""
+import sys, numpy as np, paper_2504_11681_b200 as T
+from oracle import fnofuse_port as O
+res = {}
+# the tuned geometries (C3 / C5 planes, 128^2 keep 16) with more planes than CTAs, and the
+# spectrum API (the forward kernel's modes alone)
+for s in [(40, 8, 5, 256, 256, 32, 32), (80, 4, 3, 256, 256, 16, 16), (64, 5, 2, 128, 128, 16, 16),
+          (1, 3, 2, 256, 256, 32, 32)]:
+    cfg = T.FnoLayerConfig(*s, rank=2)
+    x, w = O.random_inputs(cfg, 11 + s[0])
+    out, _ = T.run_fused(cfg, T.SpectralTensor(x), T.ComplexMatrix(w))
+    res[str(s)] = out.data
+np.savez(sys.argv[1], **res)
+print("ok")
+"""
+
+
+def test_forward_skewed_class_tail_bitwise(tmp_path):
+    """The tuned forward's software-pipelined class tail (TFNO_PLANE_SKEW=1,
+    default: column pass 1 of class c-1 and pass 2 of class c-2 beside the rows
+    of class c, one barrier per class) runs the same operations in the same
+    order as the three-barrier tail (TFNO_PLANE_SKEW=0): bitwise-equal layers."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("0", "1"):
+        f = str(tmp_path / f"skew{v}.npz")
+        env = dict(os.environ, TFNO_PLANE_SKEW=v, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", _SKEW_CODE, f], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+        outs.append(np.load(f))
+    for k in outs[0].files:
+        assert np.array_equal(outs[0][k], outs[1][k]), k

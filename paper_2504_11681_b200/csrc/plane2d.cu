@@ -410,7 +410,12 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
 // ============================================================== inverse
 // Row teams run decoupled (team barriers only); each team's elected thread
 // TMA-stores its own finished rows from a per-team staging ring.
-template <class G, int SO, bool NATURAL, bool DST>
+// SKEW: the class head is software-pipelined like the forward's tail — while the
+// rows of class c are written, the column pass 2 of class c+1 and pass 1 of class
+// c+2 run on their own class buffers (three), the mode tile is double-buffered
+// (the next plane's tile lands while this plane's last classes run), one
+// compute-wide barrier per class instead of three.  Same operations, same order.
+template <class G, int SO, bool NATURAL, bool DST, bool SKEW = false>
 __global__ void __launch_bounds__(G::NTH, 1)
     plane_inv2d_kernel(const float2* __restrict__ Cin, float2* __restrict__ y, int64_t planes,
                        const float2* __restrict__ twg, float scale) {
@@ -418,12 +423,12 @@ __global__ void __launch_bounds__(G::NTH, 1)
   constexpr int KX = G::KX, KY = G::KY, DX = G::DX, IPC = G::IPC, TS = G::TS, NTH = G::NTH;
   extern __shared__ __align__(128) uint8_t smem[];
   float2* ost = reinterpret_cast<float2*>(smem);  // TEAMS x SO x NY (TMA store sources; unused if DST)
-  float2* cin = ost + (DST ? 0 : TEAMS * SO * NY);  // KX*KY (TMA load target)
-  float2* Gb = cin + KX * KY;                     // KX*KY
-  float2* tr = Gb + KX * KY;
+  float2* cin = ost + (DST ? 0 : TEAMS * SO * NY);  // KX*KY (TMA load target; SKEW: two)
+  float2* Gb = cin + (SKEW ? 2 : 1) * KX * KY;      // KX*KY (SKEW: three class buffers)
+  float2* tr = Gb + (SKEW ? 3 : 1) * KX * KY;
   float2* twy = tr + TEAMS * 8 * TS;
   float2* twx = twy + NY;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(twx + DX);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(twx + DX);  // SKEW: two (one per mode-tile buffer)
 
   const int tid = threadIdx.x;
   const int team = tid / M, tt = tid % M;
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
   for (int k = tid; k < DX; k += NTH) twx[k] = cscale(conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DX)])), scale);
   if (tid == 0) {
     mbar_init(bar, 1);
+    if (SKEW) mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -441,10 +447,12 @@ __global__ void __launch_bounds__(G::NTH, 1)
   const uint64_t pol = policy_evict_first();
   auto issue = [&](int64_t k) {
     const int64_t pl = blockIdx.x + k * gridDim.x;
-    mbar_expect_tx(bar, KX * KY * 8);
-    tma_load_1d(cin, Cin + pl * (int64_t)KX * KY, KX * KY * 8, bar, pol);
+    const int b = SKEW ? (int)(k & 1) : 0;
+    mbar_expect_tx(bar + b, KX * KY * 8);
+    tma_load_1d(cin + b * (KX * KY), Cin + pl * (int64_t)KX * KY, KX * KY * 8, bar + b, pol);
   };
   if (tid == 0 && nmine > 0) issue(0);
+  if (SKEW && tid == 0 && nmine > 1) issue(1);
 
   float2* trt = tr + team * 8 * TS;
   float2* ostt = ost + team * SO * NY;
@@ -456,41 +464,13 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
   for (int t = 0; t < 8; ++t) tw2[t] = twy[(8 * t * a_) % NY];
   int oslot = 0;  // team-local staging-ring slot (row iteration mod SO, kept incrementally)
-  for (int64_t k = 0; k < nmine; ++k) {
-    mbar_wait(bar, (uint32_t)(k & 1));
-    const int64_t pl = blockIdx.x + k * gridDim.x;
-    float2* yp = y + pl * (int64_t)DX * NY;
-    for (int x0 = 0; x0 < R; ++x0) {
-      named_bar(kComputeBar, NTH);  // previous class's rows are done with Gb
-      // ---- column iFFT, pass 1: twiddle w_dx^{+p x0}, radix KA over u
-      for (int tau = tid; tau < 8 * KY; tau += NTH) {
-        const int q = tau % KY, s2 = tau / KY;
-        float2 w[KA];
-        const int qi = NATURAL ? (q / T) + 8 * (q % T) : q;
-#pragma unroll
-        for (int u = 0; u < KA; ++u) {
-          const int p = s2 + 8 * u;
-          w[u] = cmul(cin[p * KY + qi], twx[p * x0]);  // twx carries the output scale
-        }
-        dft_small<KA, 1>(w);
-#pragma unroll
-        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twy[s2 * i * (NY / KX)]);
-#pragma unroll
-        for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KY + q] = w[i];
-      }
-      named_bar(kComputeBar, NTH);
-      if (x0 == R - 1 && tid == 0 && k + 1 < nmine) issue(k + 1);  // cin fully consumed
-      // pass 2: radix 8 over s -> rows x1 = i + KA*m (in place per task)
-      for (int tau = tid; tau < KA * KY; tau += NTH) {
-        const int q = tau % KY, i = tau / KY;
-        float2 v[8];
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) v[s2] = Gb[(s2 * KA + i) * KY + q];
-        dft8<1>(v);
-#pragma unroll
-        for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KY + q] = v[m];
-      }
-      named_bar(kComputeBar, NTH);
+  if constexpr (SKEW) {
+    const int64_t NCL = nmine * R;
+    // rows of class c (team-decoupled), from class buffer Gc
+    auto rows_of = [&](int64_t cl) {
+      const float2* Gc = Gb + (int)(cl % 3) * (KX * KY);
+      const int x0 = (int)(cl % R);
+      float2* yp = y + (blockIdx.x + (cl / R) * gridDim.x) * (int64_t)DX * NY;
       for (int j = 0; j < IPC; ++j, oslot = (oslot + 1 == SO ? 0 : oslot + 1)) {
         const int x1 = j * TEAMS + team;
         // ---- row stage A: twiddle w_M^{+t a}, radix 8 over t (t < T nonzero)
@@ -499,7 +479,7 @@ __global__ void __launch_bounds__(G::NTH, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             if (t < T) {
-              float2 g = Gb[x1 * KY + t + T * r_];  // storage column q' = t + T*r
+              float2 g = Gc[x1 * KY + t + T * r_];  // storage column q' = t + T*r
               u[t] = t ? cmul(g, tw2[t]) : g;
             } else {
               u[t] = make_float2(0.f, 0.f);
@@ -538,6 +518,145 @@ __global__ void __launch_bounds__(G::NTH, 1)
           bulk_commit();
         }
       }
+    };
+    auto pass1_of = [&](int64_t c) {  // twiddle w_dx^{+p x0} (x output scale), radix KA over u
+      const int64_t k = c / R;
+      const int x0 = (int)(c % R);
+      if (x0 == 0) mbar_wait(bar + (k & 1), (uint32_t)((k >> 1) & 1));
+      const float2* ci = cin + (int)(k & 1) * (KX * KY);
+      float2* G1 = Gb + (int)(c % 3) * (KX * KY);
+      for (int tau = tid; tau < 8 * KY; tau += NTH) {
+        const int q = tau % KY, s2 = tau / KY;
+        float2 w[KA];
+        const int qi = NATURAL ? (q / T) + 8 * (q % T) : q;
+#pragma unroll
+        for (int u = 0; u < KA; ++u) {
+          const int p = s2 + 8 * u;
+          w[u] = cmul(ci[p * KY + qi], twx[p * x0]);
+        }
+        dft_small<KA, 1>(w);
+#pragma unroll
+        for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twy[s2 * i * (NY / KX)]);
+#pragma unroll
+        for (int i = 0; i < KA; ++i) G1[(s2 * KA + i) * KY + q] = w[i];
+      }
+    };
+    auto pass2_of = [&](int64_t c) {  // radix 8 over s -> rows x1 = i + KA*m (in place per task)
+      float2* G2 = Gb + (int)(c % 3) * (KX * KY);
+      for (int tau = tid; tau < KA * KY; tau += NTH) {
+        const int q = tau % KY, i = tau / KY;
+        float2 v[8];
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) v[s2] = G2[(s2 * KA + i) * KY + q];
+        dft8<1>(v);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) G2[(i + KA * m) * KY + q] = v[m];
+      }
+    };
+    // after the barrier that completes pass 1 of class c: the last class of plane k
+    // frees mode-tile buffer k&1 for plane k+2
+    auto refill = [&](int64_t c) {
+      if (tid == 0 && c >= 0 && c < NCL && (int)(c % R) == R - 1 && c / R + 2 < nmine) issue(c / R + 2);
+    };
+    if (NCL > 0) pass1_of(0);
+    named_bar(kComputeBar, NTH);
+    refill(0);
+    if (NCL > 0) pass2_of(0);
+    if (NCL > 1) pass1_of(1);
+    named_bar(kComputeBar, NTH);
+    refill(1);
+#pragma unroll 1
+    for (int64_t c = 0; c < NCL; ++c) {
+      rows_of(c);
+      if (c + 1 < NCL) pass2_of(c + 1);
+      if (c + 2 < NCL) pass1_of(c + 2);
+      named_bar(kComputeBar, NTH);
+      refill(c + 2);
+    }
+  } else {
+    for (int64_t k = 0; k < nmine; ++k) {
+      mbar_wait(bar, (uint32_t)(k & 1));
+      const int64_t pl = blockIdx.x + k * gridDim.x;
+      float2* yp = y + pl * (int64_t)DX * NY;
+      for (int x0 = 0; x0 < R; ++x0) {
+        named_bar(kComputeBar, NTH);  // previous class's rows are done with Gb
+        // ---- column iFFT, pass 1: twiddle w_dx^{+p x0}, radix KA over u
+        for (int tau = tid; tau < 8 * KY; tau += NTH) {
+          const int q = tau % KY, s2 = tau / KY;
+          float2 w[KA];
+          const int qi = NATURAL ? (q / T) + 8 * (q % T) : q;
+  #pragma unroll
+          for (int u = 0; u < KA; ++u) {
+            const int p = s2 + 8 * u;
+            w[u] = cmul(cin[p * KY + qi], twx[p * x0]);  // twx carries the output scale
+          }
+          dft_small<KA, 1>(w);
+  #pragma unroll
+          for (int i = 1; i < KA; ++i) w[i] = cmul(w[i], twy[s2 * i * (NY / KX)]);
+  #pragma unroll
+          for (int i = 0; i < KA; ++i) Gb[(s2 * KA + i) * KY + q] = w[i];
+        }
+        named_bar(kComputeBar, NTH);
+        if (x0 == R - 1 && tid == 0 && k + 1 < nmine) issue(k + 1);  // cin fully consumed
+        // pass 2: radix 8 over s -> rows x1 = i + KA*m (in place per task)
+        for (int tau = tid; tau < KA * KY; tau += NTH) {
+          const int q = tau % KY, i = tau / KY;
+          float2 v[8];
+  #pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) v[s2] = Gb[(s2 * KA + i) * KY + q];
+          dft8<1>(v);
+  #pragma unroll
+          for (int m = 0; m < 8; ++m) Gb[(i + KA * m) * KY + q] = v[m];
+        }
+        named_bar(kComputeBar, NTH);
+        for (int j = 0; j < IPC; ++j, oslot = (oslot + 1 == SO ? 0 : oslot + 1)) {
+          const int x1 = j * TEAMS + team;
+          // ---- row stage A: twiddle w_M^{+t a}, radix 8 over t (t < T nonzero)
+          {
+            float2 u[8];
+  #pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (t < T) {
+                float2 g = Gb[x1 * KY + t + T * r_];  // storage column q' = t + T*r
+                u[t] = t ? cmul(g, tw2[t]) : g;
+              } else {
+                u[t] = make_float2(0.f, 0.f);
+              }
+            }
+            dft8<1>(u);
+  #pragma unroll
+            for (int c = 0; c < 8; ++c) trt[r_ * TS + a_ + A * c] = u[c];
+          }
+          const int slot = oslot;
+          if (!DST && elected) bulk_wait_read<SO - 1>();  // staging slot free again
+          team_sync<M>(team);
+          // ---- row stage B: twiddle w_N^{+r y1}, radix 8 over r -> staging row
+          {
+            float2 v[8];
+  #pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = trt[r * TS + tt];
+  #pragma unroll
+            for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw1[r]);
+            dft8<1>(v);
+            if (DST) {  // coalesced streaming stores straight from registers (no smem staging)
+              float2* orow = yp + (int64_t)(x0 + R * x1) * NY;
+  #pragma unroll
+              for (int y2 = 0; y2 < 8; ++y2) __stcs(orow + tt + M * y2, v[y2]);
+            } else {
+              float2* o = ostt + slot * NY;
+  #pragma unroll
+              for (int y2 = 0; y2 < 8; ++y2) o[tt + M * y2] = v[y2];
+            }
+          }
+          if (!DST) fence_proxy_async();
+          team_sync<M>(team);
+          if (!DST && elected) {
+            const int row = x0 + R * x1;
+            tma_store_1d(yp + (int64_t)row * NY, ostt + slot * NY, NY * 8, pol);
+            bulk_commit();
+          }
+        }
+      }
     }
   }
   if (!DST && elected) bulk_wait_all();
@@ -551,8 +670,8 @@ constexpr size_t fwd_smem(int S, bool dld = false, bool skew = false) {
          16 * S + 64;
 }
 template <class G>
-constexpr size_t inv_smem(int SO, bool dst = false) {
-  return sizeof(float2) * (2 * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS +
+constexpr size_t inv_smem(int SO, bool dst = false, bool skew = false) {
+  return sizeof(float2) * ((skew ? 5 : 2) * (size_t)G::KX * G::KY + G::TEAMS * 8 * G::TS +
                            (size_t)(dst ? 0 : SO) * G::TEAMS * G::NY + G::NY + G::DX) +
          16 + 64;
 }
@@ -578,14 +697,18 @@ static int plane_variant() {
 
 static int num_sms() { return device_sms(); }
 
-static int plane_skew_env() {  // TFNO_PLANE_SKEW=0 selects the three-barrier class tail (A/B)
+static int plane_skew_env() {  // TFNO_PLANE_SKEW=0/1 overrides the per-geometry default (A/B)
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("TFNO_PLANE_SKEW");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : -1;
   }
   return v;
 }
+// measured same box, alternating (profiles/r02/skew_ab.txt): C5 plane (256^2 keep 16) forward
+// 1.567 -> 1.537 ms with the pipelined tail; C3 plane (keep 32) 0.2175 -> 0.2339 ms (slower: kept off)
+template <class G>
+constexpr bool fwd_skew_default() { return G::KX == 16 && G::DX == 256; }
 
 template <class G, int S, bool NAT, bool DLD, bool SKEW>
 static cudaError_t launch_fwd_k(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
@@ -605,7 +728,8 @@ static cudaError_t launch_fwd_k(const float2* x, float2* A, int64_t planes, cons
 template <class G, int S, bool NAT, bool DLD>
 static cudaError_t launch_fwd_v(const float2* x, float2* A, int64_t planes, const float2* tw, cudaStream_t st) {
   if constexpr (fwd_skew_ok<G>()) {
-    if (plane_skew_env() != 0) return launch_fwd_k<G, S, NAT, DLD, true>(x, A, planes, tw, st);
+    const int e = plane_skew_env();
+    if (e > 0 || (e < 0 && fwd_skew_default<G>())) return launch_fwd_k<G, S, NAT, DLD, true>(x, A, planes, tw, st);
   }
   return launch_fwd_k<G, S, NAT, DLD, false>(x, A, planes, tw, st);
 }
@@ -624,20 +748,38 @@ static cudaError_t launch_fwd(const float2* x, float2* A, int64_t planes, const 
   }
 }
 
-template <class G, int SO, bool NAT, bool DST>
-static cudaError_t launch_inv_v(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale,
+template <class G, int SO, bool NAT, bool DST, bool SKEW>
+static cudaError_t launch_inv_k(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale,
                                 cudaStream_t st) {
   const int sms = num_sms();
-  size_t smem = inv_smem<G>(SO, DST);
+  size_t smem = inv_smem<G>(SO, DST, SKEW);
   int grid = (int)(planes < sms ? planes : sms);
   if (grid < 1) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, NAT, DST>,
+  cudaError_t e = cudaFuncSetAttribute(plane_inv2d_kernel<G, SO, NAT, DST, SKEW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(plane_inv2d_kernel<G, SO, NAT, DST>, dim3(grid), dim3(G::NTH), smem, st, Cm, y, planes, tw, scale);
+  e = launch_pdl(plane_inv2d_kernel<G, SO, NAT, DST, SKEW>, dim3(grid), dim3(G::NTH), smem, st, Cm, y, planes, tw, scale);
   if (e != cudaSuccess) return e;
   ++g_launches;
   return cudaGetLastError();
+}
+
+static int plane_iskew_env() {  // TFNO_PLANE_ISKEW=0 selects the three-barrier class head (A/B)
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFNO_PLANE_ISKEW");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+template <class G, int SO, bool NAT, bool DST>
+static cudaError_t launch_inv_v(const float2* Cm, float2* y, int64_t planes, const float2* tw, float scale,
+                                cudaStream_t st) {
+  if constexpr (inv_smem<G>(SO, DST, true) <= 227 * 1024) {
+    if (plane_iskew_env() != 0) return launch_inv_k<G, SO, NAT, DST, true>(Cm, y, planes, tw, scale, st);
+  }
+  return launch_inv_k<G, SO, NAT, DST, false>(Cm, y, planes, tw, scale, st);
 }
 
 template <class G, int SO>

@@ -220,13 +220,15 @@ print("ok")
 def test_forward_skewed_class_tail_bitwise(tmp_path):
     """The tuned forward's software-pipelined class tail (TFNO_PLANE_SKEW=1,
     default: column pass 1 of class c-1 and pass 2 of class c-2 beside the rows
-    of class c, one barrier per class) runs the same operations in the same
-    order as the three-barrier tail (TFNO_PLANE_SKEW=0): bitwise-equal layers."""
+    of class c, one barrier per class) and the inverse's pipelined class head
+    (TFNO_PLANE_ISKEW=1: pass 2 of class c+1 and pass 1 of class c+2 beside the
+    rows of class c, double-buffered mode tile) run the same operations in the
+    same order as the three-barrier versions (=0): bitwise-equal layers."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for v in ("0", "1"):
         f = str(tmp_path / f"skew{v}.npz")
-        env = dict(os.environ, TFNO_PLANE_SKEW=v, PYTHONPATH=root)
+        env = dict(os.environ, TFNO_PLANE_SKEW=v, TFNO_PLANE_ISKEW=v, PYTHONPATH=root)
         r = subprocess.run([sys.executable, "-c", _SKEW_CODE, f], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
         outs.append(np.load(f))

@@ -764,11 +764,14 @@ static cudaError_t launch_inv_k(const float2* Cm, float2* y, int64_t planes, con
   return cudaGetLastError();
 }
 
-static int plane_iskew_env() {  // TFNO_PLANE_ISKEW=0 selects the three-barrier class head (A/B)
+// TFNO_PLANE_ISKEW=1 selects the pipelined class head (opt-in A/B): parity-green and bitwise
+// equal, but measured slower (profiles/r02/iskew_ab.txt: C3 inverse 0.1864 -> 0.190 ms, C5 plane
+// inverse 1.492 -> 1.686 ms) — the lock-stepped row teams write more evenly than drifting ones
+static int plane_iskew_env() {
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("TFNO_PLANE_ISKEW");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 0;
   }
   return v;
 }

@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs g) {
 // complex MAC is two FFMA2 with broadcast A operands (half the issue slots of
 // the 4-FFMA form at the same FP32-pipe rate).
 template <int TI, int TJ, bool PK = false>
-__global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : 2)) cgemm_modes_kernel(GemmArgs g) {
-  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 || PK ? 8 : 16);
+__global__ void __launch_bounds__(256, (TI * TJ > 32 ? 1 : TI * TJ <= 16 ? 4 : 2)) cgemm_modes_kernel(GemmArgs g) {
+  constexpr int FBM = 16 * TI, FBN = 16 * TJ, FBK = (TI * TJ > 32 || TI * TJ <= 16 || PK ? 8 : 16);
   __shared__ __align__(16) float2 As[2][FBK][FBM];
   __shared__ __align__(16) float2 Ws[2][FBK][FBN * (PK ? 2 : 1)];
   pdl_wait();  // PDL launch: A is the previous kernel's output
@@ -506,6 +506,15 @@ static bool big_tiles() {  // TFNO_CGEMM_BIG=0 selects the 64 x 128 tile (A/B ru
   return v != 0;
 }
 
+static bool small_tiles() {  // TFNO_CGEMM_SMALL=1: 64 x 64 tiles for N <= 64 (more CTAs per wave; A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFNO_CGEMM_SMALL");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
+
 cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   const bool fast = g.a_ms == 1 && g.c_ms == 1 && g.w_ns == 1 && (g.a_ks % 2 == 0) && (g.a_bs % 2 == 0) &&
                     (g.w_ks % 2 == 0) && (g.w_bs % 2 == 0) && g.N > 16 && g.M >= 64 &&
@@ -544,6 +553,9 @@ cudaError_t launch_cgemm(const GemmArgs& g, cudaStream_t s) {
   } else if (fast && g.N > 64) {
     dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 127) / 128), (unsigned)g.batch);
     launch_pdl(cgemm_modes_kernel<4, 8>, grid, dim3(256), 0, s, g);  // packed form spills at 2 CTAs/SM
+  } else if (fast && g.M >= 128 && g.N <= 64 && small_tiles()) {
+    dim3 grid((unsigned)((g.M + 63) / 64), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
+    launch_pdl(cgemm_modes_kernel<4, 4>, grid, dim3(256), 0, s, g);
   } else if (fast && g.M >= 128) {
     dim3 grid((unsigned)((g.M + 127) / 128), (unsigned)((g.N + 63) / 64), (unsigned)g.batch);
     launch_pdl(cgemm_modes_kernel<8, 4>, grid, dim3(256), 0, s, g);

@@ -39,7 +39,7 @@ struct PGCfg {
   // forward accumulators in shared memory when they fit next to everything else (frees registers
   // for the hoisted twiddle companions; 1024 keeps registers)
   static constexpr size_t FWD_BASE = sizeof(float2) * ((size_t)S * GF::TEAMS * DY + (size_t)GF::NTB * GF::TB +
-                                                       (size_t)KP * KP + DY + KP + 1024) + 16 * S + 16;
+                                                       (size_t)KP * KP + 2 * DY + KP + 1024) + 16 * S + 16;
   static constexpr size_t ACC_BYTES = sizeof(float2) * (size_t)GF::TASKS2 * GF::KA * GF::NTH;
   static constexpr bool ACCS = !S4 && !BIG && FWD_BASE + ACC_BYTES <= 227 * 1024;
 };
@@ -47,7 +47,7 @@ struct PGCfg {
 template <class G>
 size_t g_fwd_smem(int S, bool accs, int dx) {
   return sizeof(float2) * ((size_t)S * G::TEAMS * G::DY + (size_t)G::NTB * G::TB + (size_t)G::KXP * G::KYP +
-                           (accs ? (size_t)G::TASKS2 * G::KA * G::NTH : 0) + G::DY + G::KXP + dx) +
+                           (accs ? (size_t)G::TASKS2 * G::KA * G::NTH : 0) + 2 * G::DY + G::KXP + dx) +
          16 * S + 16;
 }
 template <class G>

@@ -98,8 +98,11 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   float2* tb = ring + S * TEAMS * DY;              // NTB x TB transpose buffers
   float2* Tc = tb + G::NTB * G::TB;                // KXP x KYP class buffer
   float2* accs = Tc + KXP * KYP;                   // ACCS: TASKS2 x KA x NTH accumulators
-  float2* twy = accs + (ACCS ? G::TASKS2 * KA * NTH : 0);  // w_DY^k
-  float2* twk = twy + DY;                          // w_KXP^k
+  // w_DY^k with its FFMA2 companion (-w.y, w.x): the hoisted row twiddles load both halves
+  // from shared memory, so ptxas keeps the companions resident instead of rebuilding each one
+  // (MOV + negating FADD) before every use (~10% of this kernel's instructions)
+  float4* twy = reinterpret_cast<float4*>(accs + (ACCS ? G::TASKS2 * KA * NTH : 0));
+  float2* twk = reinterpret_cast<float2*>(twy + DY);  // w_KXP^k
   float2* twx = twk + KXP;                         // w_dx^k
   uint64_t* full = reinterpret_cast<uint64_t*>(twx + dx);
   uint64_t* empty = full + S;
@@ -108,7 +111,10 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   const int R = dx / KXP;
   const int64_t nmine = planes > blockIdx.x ? (planes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-  for (int k = tid; k < DY; k += blockDim.x) twy[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]);
+  for (int k = tid; k < DY; k += blockDim.x) {
+    const float2 w = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]);
+    twy[k] = make_float4(w.x, w.y, -w.y, w.x);
+  }
   for (int k = tid; k < KXP; k += blockDim.x) twk[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / KXP)]);
   for (int k = tid; k < dx; k += blockDim.x) twx[k] = __ldg(&twg[(size_t)k * (TFNO_TW_MAX / dx)]);
   if (tid == 0) {
@@ -152,12 +158,20 @@ __global__ void __launch_bounds__(G::NTH + 32, 1)
   // ---------------- compute threads
   const int team = tid / M, tt = tid % M;
   const int r_ = tt / A, a_ = tt % A;
+  auto twp_at = [&](int k) {
+    const float4 t = twy[k];
+#ifdef TFNO_TWP_REBUILD  // A/B: companions rebuilt from w (ptxas rematerialises them per use)
+    return make_twp(make_float2(t.x, t.y));
+#else
+    return twp{make_float2(t.x, t.y), make_float2(t.z, t.w)};
+#endif
+  };
   twp tw1[V];
 #pragma unroll
-  for (int r = 0; r < V; ++r) tw1[r] = make_twp(twy[r * tt]);
+  for (int r = 0; r < V; ++r) tw1[r] = twp_at(r * tt);
   twp tw3[T];
 #pragma unroll
-  for (int k = 0; k < T; ++k) tw3[k] = make_twp(twy[(V * k * a_) % DY]);
+  for (int k = 0; k < T; ++k) tw3[k] = twp_at((V * k * a_) % DY);
   // stage-2 output validity: lanes holding a kept bin after the reduce
   const bool st_ok = (r_ < RN) && (T >= A || (a_ % (A / (T < A ? T : A))) == 0);
 

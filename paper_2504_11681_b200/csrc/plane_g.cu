@@ -113,7 +113,7 @@ int g_invmix_depth(int H, int dx, int prec, size_t* bytes) {
   using X = MixGeo<G::KXP * G::KYP>;
   const int npass = prec == 3 ? 2 : 1, Hp = (H + 3) & ~3;
   const size_t wt = prec ? (size_t)npass * Hp * 128 : sizeof(float4) * (size_t)H * kMixGN;
-  const size_t rest = wt + sizeof(float2) * (2 * (size_t)G::KXP * G::KYP + (size_t)G::NTB * G::TB + G::DY + G::KXP + dx) +
+  const size_t rest = wt + sizeof(float2) * (2 * (size_t)G::KXP * G::KYP + (size_t)G::NTB * G::TB + 2 * G::DY + G::KXP + dx) +
                       8 * (5 + 2 * X::SA_MAX) + 8;
   const size_t chunk = sizeof(float2) * (size_t)X::HC * X::MC, cap = 227 * 1024;
   const int need = prec ? (2 * npass * X::MC * 32 + (int)chunk - 1) / (int)chunk : 3;

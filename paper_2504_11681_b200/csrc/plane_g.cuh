@@ -470,6 +470,15 @@ __global__ void __launch_bounds__(G::NTH, 1)
 constexpr int kMixThreads = 128;  // 4 mix warps
 constexpr int kMixBar = 14;       // named barrier of the mix warps
 
+// a twiddle and its companion from a (w, -w.y, w.x) shared-memory entry
+__device__ __forceinline__ twp twp_ld(float4 t) {
+#ifdef TFNO_TWP_REBUILD_INV  // A/B: companion rebuilt from w (ptxas rematerialises it per use)
+  return make_twp(make_float2(t.x, t.y));
+#else
+  return twp{make_float2(t.x, t.y), make_float2(t.z, t.w)};
+#endif
+}
+
 template <int MQ>
 struct MixGeo {
   static constexpr int MC = MQ < 512 ? MQ : 512;  // modes per chunk (128 * MI)
@@ -513,8 +522,9 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
   float2* cin = reinterpret_cast<float2*>(Wt + (size_t)(PREC ? NPASS * Hp : H) * GN);  // MQ (TMA target)
   float2* Gb = cin + MQ;                                   // MQ
   float2* tb = Gb + MQ;                                    // NTB x TB
-  float2* twy = tb + G::NTB * G::TB;
-  float2* twk = twy + DY;
+  // conj w_DY^k with its FFMA2 companion, loaded (not rebuilt per use) like the forward's
+  float4* twy = reinterpret_cast<float4*>(tb + G::NTB * G::TB);
+  float2* twk = reinterpret_cast<float2*>(twy + DY);
   float2* twx = twk + KXP;
   uint64_t* bar = reinterpret_cast<uint64_t*>(twx + dx);   // cin landed
   uint64_t* cready = bar + 1;                              // [2] C slot written (128 arrivals)
@@ -530,7 +540,10 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
   const int64_t nmine = tasks > blockIdx.x ? (tasks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   float2* myC = Cs + (int64_t)blockIdx.x * 2 * GN * MQ;  // this CTA's two task slots
 
-  for (int k = tid; k < DY; k += blockDim.x) twy[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]));
+  for (int k = tid; k < DY; k += blockDim.x) {
+    const float2 w = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / DY)]));
+    twy[k] = make_float4(w.x, w.y, -w.y, w.x);
+  }
   for (int k = tid; k < KXP; k += blockDim.x) twk[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / KXP)]));
   for (int k = tid; k < dx; k += blockDim.x) twx[k] = conjf2(__ldg(&twg[(size_t)k * (TFNO_TW_MAX / dx)]));
   if (tid == 0) {
@@ -806,9 +819,9 @@ __global__ void __launch_bounds__(G::NTH + kMixThreads, 1)
 
   twp tw1[V], tw3[T];
 #pragma unroll
-  for (int r = 0; r < V; ++r) tw1[r] = make_twp(twy[r * tt]);
+  for (int r = 0; r < V; ++r) tw1[r] = twp_ld(twy[r * tt]);
 #pragma unroll
-  for (int k = 0; k < T; ++k) tw3[k] = make_twp(twy[(V * k * a_) % DY]);
+  for (int k = 0; k < T; ++k) tw3[k] = twp_ld(twy[(V * k * a_) % DY]);
   int buf = 0;
   uint32_t pc = 0;  // planes done (cin phase)
   for (int64_t k = 0; k < nmine; ++k) {
